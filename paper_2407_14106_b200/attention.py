@@ -1,0 +1,358 @@
+"""Host-side mirror of the reference attention operator API over the CUDA C ABI.
+
+Names, argument meaning and error behaviour follow the reference
+``gte::`` attention interface (proj/include/gte/attention.hpp:13-77,
+proj/src/attention.cpp): ``sparse_attention``, ``sparse_attention_backward``,
+``edge_sparse_attention``, ``pattern_from_graph``, ``dense_pattern``,
+``MacCounter``/``AttnResult``/``AttnGrads``. Host entries take numpy arrays and
+run through the library's host-pointer twins (synchronous, like the
+reference). ``DevicePlan`` / ``DeviceSparseAttention`` are the HBM-resident
+multi-head path used by the benchmark and the distributed layer (torch CUDA
+tensors as plumbing only).
+
+Every call lands in libgte_b200.so; there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._lib import ConfigError, DataError, check
+
+# --------------------------------------------------------------------------
+# pattern / graph containers (reference attention.hpp:13-23, graph.hpp:17-31)
+# --------------------------------------------------------------------------
+
+
+@dataclass
+class Graph:
+    num_nodes: int
+    row_offsets: np.ndarray
+    col_indices: np.ndarray
+
+    def nnz(self) -> int:
+        return int(self.col_indices.shape[0])
+
+    def neighbors(self, u: int) -> np.ndarray:
+        return self.col_indices[self.row_offsets[u]:self.row_offsets[u + 1]]
+
+
+@dataclass
+class AttnPattern:
+    rows: int
+    row_offsets: np.ndarray
+    cols: np.ndarray
+
+    def nnz(self) -> int:
+        return int(self.cols.shape[0])
+
+    def row_cols(self, r: int) -> np.ndarray:
+        return self.cols[self.row_offsets[r]:self.row_offsets[r + 1]]
+
+
+def pattern_from_graph(g: Graph) -> AttnPattern:
+    """reference proj/src/attention.cpp:26-32"""
+    return AttnPattern(g.num_nodes, np.asarray(g.row_offsets, np.int64), np.asarray(g.col_indices, np.int64))
+
+
+def dense_pattern(n: int) -> AttnPattern:
+    """reference proj/src/attention.cpp:34-44 (materialises n^2 pairs; small n only)."""
+    ro = np.arange(n + 1, dtype=np.int64) * n
+    cols = np.tile(np.arange(n, dtype=np.int64), n)
+    return AttnPattern(n, ro, cols)
+
+
+@dataclass
+class MacCounter:
+    score_macs: int = 0
+    weight_macs: int = 0
+
+    def __iadd__(self, o: "MacCounter"):
+        self.score_macs += o.score_macs
+        self.weight_macs += o.weight_macs
+        return self
+
+
+@dataclass
+class AttnResult:
+    output: np.ndarray
+    macs: MacCounter = field(default_factory=MacCounter)
+
+
+@dataclass
+class AttnGrads:
+    dq: np.ndarray
+    dk: np.ndarray
+    dv: np.ndarray
+    dbias: np.ndarray
+
+
+# --------------------------------------------------------------------------
+# context + plans
+# --------------------------------------------------------------------------
+
+
+class Context:
+    """gte_ctx for one device (device, stream, workspaces, latched errors)."""
+
+    _by_device: dict[int, "Context"] = {}
+
+    def __init__(self, device: int = 0):
+        L = _lib.lib()
+        h = C.c_void_p()
+        check(L.gte_ctx_create(device, C.byref(h)))
+        self.h = h
+        self.device = device
+
+    @classmethod
+    def get(cls, device: int = 0) -> "Context":
+        if device not in cls._by_device:
+            cls._by_device[device] = Context(device)
+        return cls._by_device[device]
+
+    def set_stream(self, stream_handle: int | None) -> None:
+        _lib.lib().gte_ctx_set_stream(self.h, C.c_void_p(stream_handle or 0))
+
+    def sync(self) -> None:
+        check(_lib.lib().gte_ctx_sync(self.h))
+
+    @property
+    def launches(self) -> int:
+        return int(_lib.lib().gte_ctx_launches(self.h))
+
+
+class DevicePlan:
+    """gte_plan: the pattern resident in HBM as int32 CSR + CSC."""
+
+    def __init__(self, handle: C.c_void_p, ctx: Context):
+        self.h = handle
+        self.ctx = ctx
+        rows, nnz, mr, mc = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+        _lib.lib().gte_plan_shape(handle, C.byref(rows), C.byref(nnz), C.byref(mr), C.byref(mc))
+        self.rows, self.nnz = rows.value, nnz.value
+        self.max_row_deg, self.max_col_deg = mr.value, mc.value
+
+    @classmethod
+    def from_host(cls, row_offsets, cols, ctx: Context | None = None) -> "DevicePlan":
+        ctx = ctx or Context.get()
+        ro = np.ascontiguousarray(row_offsets, dtype=np.int64)
+        co = np.ascontiguousarray(cols, dtype=np.int64)
+        if co.shape[0] == 0:
+            co = np.zeros(1, dtype=np.int64)
+            nnz = 0
+        else:
+            nnz = co.shape[0]
+        h = C.c_void_p()
+        check(_lib.lib().gte_plan_create_host(ctx.h, ro.shape[0] - 1, nnz, ro.ctypes.data, co.ctypes.data, C.byref(h)))
+        return cls(h, ctx)
+
+    @classmethod
+    def from_pattern(cls, pat: AttnPattern, ctx: Context | None = None) -> "DevicePlan":
+        return cls.from_host(pat.row_offsets, pat.cols, ctx)
+
+    @classmethod
+    def from_device(cls, rows: int, nnz: int, row_ptr_ptr: int, cols_ptr: int, ctx: Context | None = None):
+        ctx = ctx or Context.get()
+        h = C.c_void_p()
+        check(_lib.lib().gte_plan_create_device(ctx.h, rows, nnz, C.c_void_p(row_ptr_ptr), C.c_void_p(cols_ptr),
+                                                C.byref(h)))
+        return cls(h, ctx)
+
+    def close(self):
+        if self.h:
+            _lib.lib().gte_plan_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# --------------------------------------------------------------------------
+# reference-shaped host API (one head per call, like the reference)
+# --------------------------------------------------------------------------
+
+_NP = {"f64": np.float64, "f32": np.float32}
+
+
+def _check_shapes(q, k, v):
+    # reference proj/src/attention.cpp:12-18
+    if q.shape[0] != k.shape[0] or q.shape[0] != v.shape[0]:
+        raise ConfigError("attention: Q/K/V row counts differ")
+    if q.shape[1] != k.shape[1]:
+        raise ConfigError("attention: Q/K column counts differ")
+    if q.shape[1] < 1:
+        raise ConfigError("attention: d_K must be >= 1")
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data
+
+
+def _prep(a, dt):
+    return None if a is None else np.ascontiguousarray(a, dtype=dt)
+
+
+def sparse_attention(q, k, v, pat: AttnPattern, bias=None, weight_mult=None, forbid_empty_rows: bool = False,
+                     *, dtype: str = "f64", plan: DevicePlan | None = None, return_lse: bool = False):
+    """reference proj/src/attention.cpp:96-162 (fp64 conformance by default)."""
+    q, k, v = (np.asarray(x) for x in (q, k, v))
+    _check_shapes(q, k, v)
+    if pat.rows != q.shape[0]:
+        raise ConfigError("sparse_attention: pattern/sequence length mismatch")
+    if bias is not None and len(bias) and len(bias) != pat.nnz():
+        raise ConfigError("sparse_attention: bias must cover exactly the attended pairs")
+    if weight_mult is not None and len(weight_mult) and len(weight_mult) != pat.nnz():
+        raise ConfigError("sparse_attention: weight_mult size mismatch")
+    bias = None if bias is None or len(bias) == 0 else bias
+    weight_mult = None if weight_mult is None or len(weight_mult) == 0 else weight_mult
+    dt = _NP[dtype]
+    S, dk = q.shape
+    dv = v.shape[1]
+    qq, kk, vv = _prep(q, dt), _prep(k, dt), _prep(v, dt)
+    b, w = _prep(bias, dt), _prep(weight_mult, dt)
+    plan = plan or DevicePlan.from_pattern(pat)
+    out = np.zeros((S, dv), dtype=dt)
+    lse = np.zeros((S, 1), dtype=dt)
+    if S > 0:
+        check(_lib.lib().gte_sparse_attn_fwd_host(plan.ctx.h, plan.h, _lib.DTYPES[dtype], 1, dk, dv, qq.ctypes.data,
+                                                  kk.ctypes.data, vv.ctypes.data, _ptr(b), _ptr(w), out.ctypes.data,
+                                                  lse.ctypes.data, _lib.GTE_FORBID_EMPTY_ROWS if forbid_empty_rows else 0))
+    res = AttnResult(out, MacCounter(pat.nnz() * dk, pat.nnz() * dv))
+    if return_lse:
+        return res, lse
+    return res
+
+
+def sparse_attention_backward(q, k, v, pat: AttnPattern, bias, weight_mult, upstream, *, dtype: str = "f64",
+                              plan: DevicePlan | None = None) -> AttnGrads:
+    """reference proj/src/attention.cpp:241-320"""
+    q, k, v, upstream = (np.asarray(x) for x in (q, k, v, upstream))
+    _check_shapes(q, k, v)
+    S, dk = q.shape
+    dv = v.shape[1]
+    if pat.rows != S:
+        raise ConfigError("sparse_attention_backward: pattern mismatch")
+    if upstream.shape != (S, dv):
+        raise ConfigError("sparse_attention_backward: upstream shape mismatch")
+    bias = None if bias is None or len(bias) == 0 else bias
+    weight_mult = None if weight_mult is None or len(weight_mult) == 0 else weight_mult
+    dt = _NP[dtype]
+    plan = plan or DevicePlan.from_pattern(pat)
+    # the softmax statistics come from a forward through the same kernels
+    # (the reference recomputes them inside its backward, attention.cpp:275-290)
+    fwd, lse = _forward_nocheck(q, k, v, plan, bias, weight_mult, dtype)
+    qq, kk, vv, uu = (_prep(x, dt) for x in (q, k, v, upstream))
+    b, w = _prep(bias, dt), _prep(weight_mult, dt)
+    dq, dkk, dvv = np.zeros((S, dk), dt), np.zeros((S, dk), dt), np.zeros((S, dv), dt)
+    db = np.zeros(max(pat.nnz(), 1), dt)
+    if S > 0:
+        check(_lib.lib().gte_sparse_attn_bwd_host(plan.ctx.h, plan.h, _lib.DTYPES[dtype], 1, dk, dv, qq.ctypes.data,
+                                                  kk.ctypes.data, vv.ctypes.data, fwd.ctypes.data, lse.ctypes.data,
+                                                  uu.ctypes.data, _ptr(b), _ptr(w), dq.ctypes.data, dkk.ctypes.data,
+                                                  dvv.ctypes.data, db.ctypes.data))
+    return AttnGrads(dq, dkk, dvv, db[:pat.nnz()])
+
+
+def _forward_nocheck(q, k, v, plan, bias, wm, dtype):
+    dt = _NP[dtype]
+    S, dk = q.shape
+    dv = v.shape[1]
+    qq, kk, vv = _prep(q, dt), _prep(k, dt), _prep(v, dt)
+    out = np.zeros((S, dv), dt)
+    lse = np.zeros((S, 1), dt)
+    if S > 0:
+        rc = _lib.lib().gte_sparse_attn_fwd_host(plan.ctx.h, plan.h, _lib.DTYPES[dtype], 1, dk, dv, qq.ctypes.data,
+                                                 kk.ctypes.data, vv.ctypes.data, _ptr(_prep(bias, dt)),
+                                                 _ptr(_prep(wm, dt)), out.ctypes.data, lse.ctypes.data, 0)
+        if rc == _lib.GTE_DATA:
+            # the reference backward performs no finiteness check
+            # (attention.cpp:241-320); NaNs simply propagate
+            pass
+        else:
+            check(rc)
+    return out, lse
+
+
+def edge_sparse_attention(q, k, v, g: Graph, bias=None, weight_mult=None, **kw) -> AttnResult:
+    """reference proj/src/attention.cpp:164-172"""
+    if g.num_nodes != np.asarray(q).shape[0]:
+        raise ConfigError("edge_sparse_attention: graph/sequence length mismatch")
+    return sparse_attention(q, k, v, pattern_from_graph(g), bias, weight_mult, forbid_empty_rows=True, **kw)
+
+
+# --------------------------------------------------------------------------
+# HBM-resident multi-head path (torch CUDA tensors are plumbing only)
+# --------------------------------------------------------------------------
+
+_TORCH_DT = {"f64": "float64", "f32": "float32", "bf16": "bfloat16"}
+
+
+class DeviceSparseAttention:
+    """All heads of one attention sublayer over a DevicePlan.
+
+    q/k: [S, H*dk], v/out/dout: [S, H*dv] CUDA tensors of `dtype`;
+    bias [nnz], weight_mult [H, nnz] in the accumulate type (f64 for f64,
+    else f32). Launches on torch's current stream.
+    """
+
+    def __init__(self, plan: DevicePlan, heads: int, dk: int, dv: int | None = None, dtype: str = "f32"):
+        self.plan, self.H, self.dk, self.dv, self.dtype = plan, heads, dk, dv or dk, dtype
+        self.code = _lib.DTYPES[dtype]
+
+    def _stream(self):
+        import torch
+
+        self.plan.ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+
+    def forward(self, q, k, v, bias=None, weight_mult=None, out=None, lse=None, forbid_empty_rows=False):
+        import torch
+
+        S = self.plan.rows
+        acc = torch.float64 if self.dtype == "f64" else torch.float32
+        if out is None:
+            out = torch.empty((S, self.H * self.dv), dtype=v.dtype, device=v.device)
+        if lse is None:
+            lse = torch.empty((S, self.H), dtype=acc, device=v.device)
+        self._stream()
+        check(_lib.lib().gte_sparse_attn_fwd(
+            self.plan.ctx.h, self.plan.h, self.code, self.H, self.dk, self.dv, q.data_ptr(), k.data_ptr(),
+            q.stride(0), v.data_ptr(), v.stride(0), None if bias is None else bias.data_ptr(),
+            None if weight_mult is None else weight_mult.data_ptr(), out.data_ptr(), lse.data_ptr(),
+            _lib.GTE_FORBID_EMPTY_ROWS if forbid_empty_rows else 0))
+        return out, lse
+
+    def backward(self, q, k, v, out, lse, dout, bias=None, weight_mult=None, dq=None, dk=None, dv=None, dbias=None):
+        import torch
+
+        acc = torch.float64 if self.dtype == "f64" else torch.float32
+        dq = torch.empty_like(q) if dq is None else dq
+        dk = torch.empty_like(k) if dk is None else dk
+        dv = torch.empty_like(v) if dv is None else dv
+        if dbias is None:
+            dbias = torch.empty(max(self.plan.nnz, 1), dtype=acc, device=q.device)
+        self._stream()
+        check(_lib.lib().gte_sparse_attn_bwd(
+            self.plan.ctx.h, self.plan.h, self.code, self.H, self.dk, self.dv, q.data_ptr(), k.data_ptr(),
+            q.stride(0), v.data_ptr(), v.stride(0), out.data_ptr(), lse.data_ptr(), dout.data_ptr(),
+            None if bias is None else bias.data_ptr(), None if weight_mult is None else weight_mult.data_ptr(),
+            dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), dbias.data_ptr()))
+        return dq, dk, dv, dbias
+
+    def fwd_bwd_host(self, q, k, v, dout, bias, out, dq, dk, dv, dbias):
+        """End-to-end unit with host (ideally pinned) buffers: H2D, fwd, bwd, D2H.
+        Arguments are CPU tensors/arrays exposing .data_ptr() or ctypes."""
+        def p(x):
+            if x is None:
+                return None
+            return x.data_ptr() if hasattr(x, "data_ptr") else x.ctypes.data
+
+        self._stream()
+        check(_lib.lib().gte_sparse_attn_fwd_bwd_host(
+            self.plan.ctx.h, self.plan.h, self.code, self.H, self.dk, self.dv, p(q), p(k), p(v), p(dout), p(bias),
+            p(out), p(dq), p(dk), p(dv), p(dbias)))

@@ -1,0 +1,577 @@
+// C ABI of the B200 graph-attention library (include/gte_b200.h): context,
+// device pattern plans (CSR + CSC built on the GPU with radix sort/scan), and
+// the sparse attention entries with their host-pointer twins.
+#include <climits>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cub/cub.cuh>
+
+#include "../../include/gte_b200.h"
+#include "attn_launch.cuh"
+
+using namespace gte_b200;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = (expr);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(GTE_CUDA, std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " \
+                                + __FILE__ + ":" + std::to_string(__LINE__));            \
+  } while (0)
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    cudaError_t e = cudaMalloc(&p, bytes ? bytes : 16);
+    if (e == cudaSuccess) cap = bytes;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+size_t elem_size(int dtype) { return dtype == GTE_F64 ? 8 : dtype == GTE_F32 ? 4 : 2; }
+size_t acc_size(int dtype) { return dtype == GTE_F64 ? 8 : 4; }
+
+__global__ void expand_rows_kernel(const int32_t* __restrict__ row_ptr, int64_t rows,
+                                   int32_t* __restrict__ row_of_edge) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= rows) return;
+  const int b = row_ptr[w], e = row_ptr[w + 1];
+  for (int i = b + lane; i < e; i += 32) row_of_edge[i] = (int32_t)w;
+}
+
+__global__ void count_cols_kernel(const int32_t* __restrict__ cols, int64_t nnz, int32_t* counts) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nnz; i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(counts + cols[i], 1);
+}
+
+__global__ void gather_rows_kernel(const int32_t* __restrict__ eid, const int32_t* __restrict__ row_of_edge,
+                                   int64_t nnz, int32_t* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nnz; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = row_of_edge[eid[i]];
+}
+
+__global__ void iota_kernel(int32_t* out, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int32_t)i;
+}
+
+__global__ void unref_kernel(const int32_t* __restrict__ counts, int64_t rows, int32_t* out, int32_t* n_out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += (int64_t)gridDim.x * blockDim.x)
+    if (counts[i] == 0) out[atomicAdd(n_out, 1)] = (int32_t)i;
+}
+
+__global__ void degree_kernel(const int32_t* __restrict__ ptr, int64_t rows, int32_t* deg) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += (int64_t)gridDim.x * blockDim.x)
+    deg[i] = ptr[i + 1] - ptr[i];
+}
+
+__global__ void check_csr_kernel(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ cols,
+                                 int64_t rows, int64_t nnz, int* bad) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nnz; i += (int64_t)gridDim.x * blockDim.x)
+    if (cols[i] < 0 || cols[i] >= rows) atomicOr(bad, 1);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += (int64_t)gridDim.x * blockDim.x)
+    if (row_ptr[i + 1] < row_ptr[i]) atomicOr(bad, 2);
+}
+
+unsigned grid_for(int64_t n, int block = 256) {
+  int64_t g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > 148 * 64) g = 148 * 64;
+  return (unsigned)g;
+}
+
+}  // namespace
+
+struct gte_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int* d_err = nullptr;  // [0] non-finite bits, [1] first empty row
+  int* h_err = nullptr;  // pinned mirror
+  int64_t launches = 0;
+  DevBuf io[12];
+};
+
+struct gte_plan {
+  gte_ctx* ctx = nullptr;
+  int64_t rows = 0, nnz = 0, max_row_deg = 0, max_col_deg = 0, n_unref = 0;
+  int32_t* row_ptr = nullptr;
+  int32_t* cols = nullptr;
+  int32_t* col_ptr = nullptr;
+  int32_t* csc_row = nullptr;
+  int32_t* csc_eid = nullptr;
+  int32_t* unref = nullptr;
+};
+
+namespace {
+
+int reset_err(gte_ctx* c) {
+  const int init[2] = {0, INT_MAX};
+  CUDA_TRY(cudaMemcpyAsync(c->d_err, init, sizeof init, cudaMemcpyHostToDevice, c->stream));
+  return GTE_OK;
+}
+
+// Reads the latched device errors (synchronising), maps them to the
+// reference's DataError messages (proj/src/attention.cpp:20-22, 119-123).
+int drain_errors(gte_ctx* c) {
+  CUDA_TRY(cudaMemcpyAsync(c->h_err, c->d_err, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  const int bits = c->h_err[0], row = c->h_err[1];
+  if (bits == 0 && row == INT_MAX) return GTE_OK;
+  int rc = reset_err(c);
+  if (rc) return rc;
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (bits & 1) return fail(GTE_DATA, "attention: non-finite Q");
+  if (bits & 2) return fail(GTE_DATA, "attention: non-finite K");
+  if (bits & 4) return fail(GTE_DATA, "attention: non-finite V");
+  return fail(GTE_DATA, "sparse_attention: row " + std::to_string(row) +
+                            " attends to nothing; run add_self_loops");
+}
+
+int build_plan_device(gte_ctx* c, gte_plan* p) {
+  const int64_t rows = p->rows, nnz = p->nnz;
+  cudaStream_t st = c->stream;
+  CUDA_TRY(cudaMallocAsync(&p->col_ptr, sizeof(int32_t) * (rows + 1), st));
+  CUDA_TRY(cudaMallocAsync(&p->csc_row, sizeof(int32_t) * (nnz + 1), st));
+  CUDA_TRY(cudaMallocAsync(&p->csc_eid, sizeof(int32_t) * (nnz + 1), st));
+  CUDA_TRY(cudaMallocAsync(&p->unref, sizeof(int32_t) * (rows + 1), st));
+  int32_t *row_of_edge = nullptr, *iota = nullptr, *sorted_cols = nullptr, *counts = nullptr, *scratch = nullptr;
+  CUDA_TRY(cudaMallocAsync(&row_of_edge, sizeof(int32_t) * (nnz + 1), st));
+  CUDA_TRY(cudaMallocAsync(&iota, sizeof(int32_t) * (nnz + 1), st));
+  CUDA_TRY(cudaMallocAsync(&sorted_cols, sizeof(int32_t) * (nnz + 1), st));
+  CUDA_TRY(cudaMallocAsync(&counts, sizeof(int32_t) * (rows + 2), st));
+  CUDA_TRY(cudaMallocAsync(&scratch, sizeof(int32_t) * 4, st));
+  CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(int32_t) * (rows + 2), st));
+  CUDA_TRY(cudaMemsetAsync(scratch, 0, sizeof(int32_t) * 4, st));
+
+  check_csr_kernel<<<grid_for(nnz > rows ? nnz : rows), 256, 0, st>>>(p->row_ptr, p->cols, rows, nnz, scratch);
+  if (rows > 0) expand_rows_kernel<<<(unsigned)((rows * 32 + 255) / 256), 256, 0, st>>>(p->row_ptr, rows, row_of_edge);
+  iota_kernel<<<grid_for(nnz), 256, 0, st>>>(iota, nnz);
+  count_cols_kernel<<<grid_for(nnz), 256, 0, st>>>(p->cols, nnz, counts);
+  c->launches += 4;
+  int bits = 1;
+  while ((1LL << bits) < rows) ++bits;
+  size_t tmp_bytes = 0, tmp2 = 0, tmp3 = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, p->cols, sorted_cols, iota, p->csc_eid, (int)nnz, 0, bits, st);
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp2, counts, p->col_ptr, (int)(rows + 1), st);
+  cub::DeviceReduce::Max(nullptr, tmp3, counts, scratch + 2, (int)rows, st);
+  if (tmp2 > tmp_bytes) tmp_bytes = tmp2;
+  if (tmp3 > tmp_bytes) tmp_bytes = tmp3;
+  void* tmp = nullptr;
+  CUDA_TRY(cudaMallocAsync(&tmp, tmp_bytes + 16, st));
+  if (nnz > 0) CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, p->cols, sorted_cols, iota, p->csc_eid, (int)nnz, 0, bits, st));
+  gather_rows_kernel<<<grid_for(nnz), 256, 0, st>>>(p->csc_eid, row_of_edge, nnz, p->csc_row);
+  unref_kernel<<<grid_for(rows), 256, 0, st>>>(counts, rows, p->unref, scratch + 1);
+  size_t tb = tmp_bytes;
+  if (rows > 0) CUDA_TRY(cub::DeviceReduce::Max(tmp, tb, counts, scratch + 2, (int)rows, st));
+  tb = tmp_bytes;
+  CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, counts, p->col_ptr, (int)(rows + 1), st));
+  degree_kernel<<<grid_for(rows), 256, 0, st>>>(p->row_ptr, rows, row_of_edge);  // reuse as row degrees
+  tb = tmp_bytes;
+  if (rows > 0) CUDA_TRY(cub::DeviceReduce::Max(tmp, tb, row_of_edge, scratch + 3, (int)rows, st));
+  c->launches += 8;
+  int32_t h[4] = {0, 0, 0, 0};
+  CUDA_TRY(cudaMemcpyAsync(h, scratch, sizeof h, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  cudaFreeAsync(tmp, st);
+  cudaFreeAsync(row_of_edge, st);
+  cudaFreeAsync(iota, st);
+  cudaFreeAsync(sorted_cols, st);
+  cudaFreeAsync(counts, st);
+  cudaFreeAsync(scratch, st);
+  if (h[0] & 1) return fail(GTE_CONFIG, "sparse_attention: pattern column out of range");
+  if (h[0] & 2) return fail(GTE_CONFIG, "sparse_attention: pattern row offsets not monotone");
+  p->n_unref = h[1];
+  p->max_col_deg = rows > 0 ? h[2] : 0;
+  p->max_row_deg = rows > 0 ? h[3] : 0;
+  return GTE_OK;
+}
+
+void free_plan(gte_plan* p) {
+  if (!p) return;
+  cudaFree(p->row_ptr);
+  cudaFree(p->cols);
+  cudaFree(p->col_ptr);
+  cudaFree(p->csc_row);
+  cudaFree(p->csc_eid);
+  cudaFree(p->unref);
+  delete p;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+int pick_dht(int d) { return d <= 8 ? 8 : d <= 16 ? 16 : d <= 32 ? 32 : 64; }
+int pick_lpn(int H) {
+  int l = 1;
+  while (l < H) l <<= 1;
+  return l;
+}
+
+cudaError_t dispatch(int dtype, int which, const SparseArgs& a, int dht, int lpn, cudaStream_t st) {
+  switch (dtype) {
+    case GTE_F64: return launch_sparse_f64(which, a, dht, lpn, st);
+    case GTE_F32: return launch_sparse_f32(which, a, dht, lpn, st);
+    default: return launch_sparse_bf16(which, a, dht, lpn, st);
+  }
+}
+
+int check_attn_args(const gte_plan* plan, int dtype, int H, int dk, int dv, int64_t ldq, int64_t ldv) {
+  if (!plan) return fail(GTE_CONFIG, "sparse_attention: null plan");
+  if (dtype != GTE_F64 && dtype != GTE_F32 && dtype != GTE_BF16) return fail(GTE_CONFIG, "sparse_attention: bad dtype");
+  if (dk < 1) return fail(GTE_CONFIG, "attention: d_K must be >= 1");
+  if (dv < 1) return fail(GTE_CONFIG, "attention: d_V must be >= 1");
+  if (dk > 64 || dv > 64) return fail(GTE_CONFIG, "sparse_attention: head dim > 64 unsupported");
+  if (H < 1 || H > 32) return fail(GTE_CONFIG, "sparse_attention: heads must lie in [1, 32]");
+  if (ldq < (int64_t)H * dk || ldv < (int64_t)H * dv) return fail(GTE_CONFIG, "sparse_attention: leading dimension too small");
+  return GTE_OK;
+}
+
+void fill_common(SparseArgs& a, const gte_plan* plan, int dtype, int H, int dk, int dv, int64_t ldq, int64_t ldv) {
+  a.S = plan->rows;
+  a.E = plan->nnz;
+  a.H = H;
+  a.dk = dk;
+  a.dv = dv;
+  a.ldq = ldq;
+  a.ldv = ldv;
+  a.row_ptr = plan->row_ptr;
+  a.cols = plan->cols;
+  a.col_ptr = plan->col_ptr;
+  a.csc_row = plan->csc_row;
+  a.csc_eid = plan->csc_eid;
+  a.scale = 1.0 / std::sqrt((double)dk);
+  a.err = plan->ctx->d_err;
+  (void)dtype;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* gte_last_error(void) { return g_err.c_str(); }
+const char* gte_version(void) { return "gte_b200 0.1 (sm_100a)"; }
+
+int gte_ctx_create(int device, gte_ctx** out) {
+  CUDA_TRY(cudaSetDevice(device));
+  auto* c = new gte_ctx();
+  c->device = device;
+  c->stream = nullptr;  // legacy default stream until set
+  CUDA_TRY(cudaMalloc(&c->d_err, 2 * sizeof(int)));
+  CUDA_TRY(cudaMallocHost(&c->h_err, 2 * sizeof(int)));
+  int rc = reset_err(c);
+  if (rc) return rc;
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  *out = c;
+  return GTE_OK;
+}
+
+int gte_ctx_destroy(gte_ctx* c) {
+  if (!c) return GTE_OK;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (auto& b : c->io) b.release();
+  cudaFree(c->d_err);
+  cudaFreeHost(c->h_err);
+  delete c;
+  return GTE_OK;
+}
+
+int gte_ctx_set_stream(gte_ctx* c, void* s) {
+  c->stream = static_cast<cudaStream_t>(s);
+  return GTE_OK;
+}
+
+int gte_ctx_sync(gte_ctx* c) { return drain_errors(c); }
+
+int64_t gte_ctx_launches(const gte_ctx* c) { return c->launches; }
+
+int gte_plan_create_device(gte_ctx* c, int64_t rows, int64_t nnz, const int32_t* d_row_ptr,
+                           const int32_t* d_cols, gte_plan** out) {
+  if (rows < 0 || nnz < 0) return fail(GTE_CONFIG, "plan: negative size");
+  if (rows >= INT_MAX || nnz >= INT_MAX) return fail(GTE_CONFIG, "plan: pattern exceeds int32 device index range");
+  auto* p = new gte_plan();
+  p->ctx = c;
+  p->rows = rows;
+  p->nnz = nnz;
+  cudaStream_t st = c->stream;
+  if (cudaMallocAsync(&p->row_ptr, sizeof(int32_t) * (rows + 1), st) != cudaSuccess ||
+      cudaMallocAsync(&p->cols, sizeof(int32_t) * (nnz + 1), st) != cudaSuccess) {
+    free_plan(p);
+    return fail(GTE_CUDA, "plan: device allocation failed");
+  }
+  cudaMemcpyAsync(p->row_ptr, d_row_ptr, sizeof(int32_t) * (rows + 1), cudaMemcpyDeviceToDevice, st);
+  if (nnz) cudaMemcpyAsync(p->cols, d_cols, sizeof(int32_t) * nnz, cudaMemcpyDeviceToDevice, st);
+  int rc = build_plan_device(c, p);
+  if (rc) {
+    free_plan(p);
+    return rc;
+  }
+  *out = p;
+  return GTE_OK;
+}
+
+int gte_plan_create_host(gte_ctx* c, int64_t rows, int64_t nnz, const int64_t* row_off,
+                         const int64_t* cols, gte_plan** out) {
+  if (rows < 0 || nnz < 0) return fail(GTE_CONFIG, "plan: negative size");
+  if (rows >= INT_MAX || nnz >= INT_MAX) return fail(GTE_CONFIG, "plan: pattern exceeds int32 device index range");
+  if (row_off[0] != 0 || row_off[rows] != nnz) return fail(GTE_CONFIG, "sparse_attention: malformed pattern offsets");
+  std::vector<int32_t> ro(rows + 1), co(nnz > 0 ? nnz : 1);
+  for (int64_t i = 0; i <= rows; ++i) ro[i] = (int32_t)row_off[i];
+  for (int64_t i = 0; i < nnz; ++i) co[i] = (int32_t)cols[i];
+  auto* p = new gte_plan();
+  p->ctx = c;
+  p->rows = rows;
+  p->nnz = nnz;
+  cudaStream_t st = c->stream;
+  if (cudaMalloc(&p->row_ptr, sizeof(int32_t) * (rows + 1)) != cudaSuccess ||
+      cudaMalloc(&p->cols, sizeof(int32_t) * (nnz + 1)) != cudaSuccess) {
+    free_plan(p);
+    return fail(GTE_CUDA, "plan: device allocation failed");
+  }
+  cudaMemcpyAsync(p->row_ptr, ro.data(), sizeof(int32_t) * (rows + 1), cudaMemcpyHostToDevice, st);
+  if (nnz) cudaMemcpyAsync(p->cols, co.data(), sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, st);
+  int rc = build_plan_device(c, p);  // synchronises before `ro`/`co` go out of scope
+  if (rc) {
+    free_plan(p);
+    return rc;
+  }
+  *out = p;
+  return GTE_OK;
+}
+
+int gte_plan_destroy(gte_plan* p) {
+  if (p) cudaStreamSynchronize(p->ctx->stream);
+  free_plan(p);
+  return GTE_OK;
+}
+
+int gte_plan_shape(const gte_plan* p, int64_t* rows, int64_t* nnz, int64_t* mr, int64_t* mc) {
+  if (rows) *rows = p->rows;
+  if (nnz) *nnz = p->nnz;
+  if (mr) *mr = p->max_row_deg;
+  if (mc) *mc = p->max_col_deg;
+  return GTE_OK;
+}
+
+int gte_plan_device_csr(const gte_plan* p, const int32_t** rp, const int32_t** cl) {
+  *rp = p->row_ptr;
+  *cl = p->cols;
+  return GTE_OK;
+}
+
+int gte_sparse_attn_fwd(gte_ctx* c, const gte_plan* plan, int dtype, int H, int dk, int dv,
+                        const void* q, const void* k, int64_t ldq, const void* v, int64_t ldv,
+                        const void* bias, const void* wmult, void* out, void* lse, int flags) {
+  int rc = check_attn_args(plan, dtype, H, dk, dv, ldq, ldv);
+  if (rc) return rc;
+  SparseArgs a;
+  fill_common(a, plan, dtype, H, dk, dv, ldq, ldv);
+  a.q = q;
+  a.k = k;
+  a.v = v;
+  a.bias = bias;
+  a.wmult = wmult;
+  a.out = out;
+  a.lse = lse;
+  a.forbid_empty = (flags & GTE_FORBID_EMPTY_ROWS) ? 1 : 0;
+  const int dht = pick_dht(dk > dv ? dk : dv), lpn = pick_lpn(H);
+  const size_t es = elem_size(dtype);
+  a.vec_qk = dk == dht && (ldq * es) % 16 == 0 && aligned16(q) && aligned16(k);
+  a.vec_v = dv == dht && (ldv * es) % 16 == 0 && aligned16(v) && aligned16(out);
+  if (plan->rows == 0) return GTE_OK;
+  CUDA_TRY(dispatch(dtype, kFwd, a, dht, lpn, c->stream));
+  c->launches += 1;
+  if (plan->n_unref > 0) {
+    CUDA_TRY(launch_finite_rows(dtype, k, v, plan->unref, (int)plan->n_unref, ldq, ldv, (int64_t)H * dk,
+                                (int64_t)H * dv, c->d_err, c->stream));
+    c->launches += 1;
+  }
+  return GTE_OK;
+}
+
+int gte_sparse_attn_bwd(gte_ctx* c, const gte_plan* plan, int dtype, int H, int dk, int dv,
+                        const void* q, const void* k, int64_t ldq, const void* v, int64_t ldv,
+                        const void* out, const void* lse, const void* dout, const void* bias,
+                        const void* wmult, void* dq, void* dk_out, void* dv_out, void* dbias) {
+  int rc = check_attn_args(plan, dtype, H, dk, dv, ldq, ldv);
+  if (rc) return rc;
+  if (plan->rows == 0) return GTE_OK;
+  DevBuf& ws = c->io[11];
+  CUDA_TRY(ws.ensure(acc_size(dtype) * (size_t)plan->rows * H));
+  SparseArgs a;
+  fill_common(a, plan, dtype, H, dk, dv, ldq, ldv);
+  a.q = q;
+  a.k = k;
+  a.v = v;
+  a.o = out;
+  a.dout = dout;
+  a.bias = bias;
+  a.wmult = wmult;
+  a.lse = const_cast<void*>(lse);
+  a.delta = ws.p;
+  a.dq = dq;
+  a.dk_out = dk_out;
+  a.dv_out = dv_out;
+  a.dbias = dbias;
+  const int dht = pick_dht(dk > dv ? dk : dv), lpn = pick_lpn(H);
+  const size_t es = elem_size(dtype);
+  a.vec_qk = dk == dht && (ldq * es) % 16 == 0 && aligned16(q) && aligned16(k) && aligned16(dq) && aligned16(dk_out);
+  a.vec_v = dv == dht && (ldv * es) % 16 == 0 && aligned16(v) && aligned16(out) && aligned16(dout) && aligned16(dv_out);
+  CUDA_TRY(dispatch(dtype, kBwdRows, a, dht, lpn, c->stream));
+  CUDA_TRY(dispatch(dtype, kBwdCols, a, dht, lpn, c->stream));
+  c->launches += 2;
+  return GTE_OK;
+}
+
+int gte_sparse_attn_fwd_host(gte_ctx* c, const gte_plan* plan, int dtype, int H, int dk, int dv,
+                             const void* q, const void* k, const void* v, const void* bias,
+                             const void* wmult, void* out, void* lse_out, int flags) {
+  int rc = check_attn_args(plan, dtype, H, dk, dv, (int64_t)H * dk, (int64_t)H * dv);
+  if (rc) return rc;
+  const size_t S = (size_t)plan->rows, E = (size_t)plan->nnz, es = elem_size(dtype), as = acc_size(dtype);
+  const size_t bq = S * H * dk * es, bv = S * H * dv * es;
+  cudaStream_t st = c->stream;
+  CUDA_TRY(c->io[0].ensure(bq));
+  CUDA_TRY(c->io[1].ensure(bq));
+  CUDA_TRY(c->io[2].ensure(bv));
+  CUDA_TRY(c->io[3].ensure(bv));
+  CUDA_TRY(c->io[4].ensure(S * H * as));
+  if (bias) CUDA_TRY(c->io[5].ensure(E * as));
+  if (wmult) CUDA_TRY(c->io[6].ensure(E * H * as));
+  CUDA_TRY(cudaMemcpyAsync(c->io[0].p, q, bq, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(c->io[1].p, k, bq, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(c->io[2].p, v, bv, cudaMemcpyHostToDevice, st));
+  if (bias) CUDA_TRY(cudaMemcpyAsync(c->io[5].p, bias, E * as, cudaMemcpyHostToDevice, st));
+  if (wmult) CUDA_TRY(cudaMemcpyAsync(c->io[6].p, wmult, E * H * as, cudaMemcpyHostToDevice, st));
+  rc = gte_sparse_attn_fwd(c, plan, dtype, H, dk, dv, c->io[0].p, c->io[1].p, (int64_t)H * dk, c->io[2].p,
+                           (int64_t)H * dv, bias ? c->io[5].p : nullptr, wmult ? c->io[6].p : nullptr,
+                           c->io[3].p, c->io[4].p, flags);
+  if (rc) return rc;
+  rc = drain_errors(c);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(out, c->io[3].p, bv, cudaMemcpyDeviceToHost, st));
+  if (lse_out) CUDA_TRY(cudaMemcpyAsync(lse_out, c->io[4].p, S * H * as, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return GTE_OK;
+}
+
+int gte_sparse_attn_bwd_host(gte_ctx* c, const gte_plan* plan, int dtype, int H, int dk, int dv,
+                             const void* q, const void* k, const void* v, const void* out,
+                             const void* lse, const void* dout, const void* bias,
+                             const void* wmult, void* dq, void* dk_out, void* dv_out, void* dbias) {
+  int rc = check_attn_args(plan, dtype, H, dk, dv, (int64_t)H * dk, (int64_t)H * dv);
+  if (rc) return rc;
+  const size_t S = (size_t)plan->rows, E = (size_t)plan->nnz, es = elem_size(dtype), as = acc_size(dtype);
+  const size_t bq = S * H * dk * es, bv = S * H * dv * es;
+  cudaStream_t st = c->stream;
+  for (int i : {0, 1, 7, 8}) CUDA_TRY(c->io[i].ensure(bq));
+  for (int i : {2, 3, 9, 10}) CUDA_TRY(c->io[i].ensure(bv));
+  CUDA_TRY(c->io[4].ensure(S * H * as));
+  CUDA_TRY(c->io[5].ensure((E + 1) * as));
+  if (wmult) CUDA_TRY(c->io[6].ensure(E * H * as));
+  CUDA_TRY(cudaMemcpyAsync(c->io[0].p, q, bq, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(c->io[1].p, k, bq, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(c->io[2].p, v, bv, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(c->io[3].p, out, bv, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(c->io[4].p, lse, S * H * as, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(c->io[9].p, dout, bv, cudaMemcpyHostToDevice, st));
+  void* dbias_dev = c->io[5].p;
+  DevBuf bias_buf;
+  const void* bias_dev = nullptr;
+  if (bias) {
+    CUDA_TRY(bias_buf.ensure(E * as));
+    CUDA_TRY(cudaMemcpyAsync(bias_buf.p, bias, E * as, cudaMemcpyHostToDevice, st));
+    bias_dev = bias_buf.p;
+  }
+  if (wmult) CUDA_TRY(cudaMemcpyAsync(c->io[6].p, wmult, E * H * as, cudaMemcpyHostToDevice, st));
+  rc = gte_sparse_attn_bwd(c, plan, dtype, H, dk, dv, c->io[0].p, c->io[1].p, (int64_t)H * dk, c->io[2].p,
+                           (int64_t)H * dv, c->io[3].p, c->io[4].p, c->io[9].p, bias_dev,
+                           wmult ? c->io[6].p : nullptr, c->io[7].p, c->io[8].p, c->io[10].p, dbias_dev);
+  if (rc == GTE_OK) {
+    CUDA_TRY(cudaMemcpyAsync(dq, c->io[7].p, bq, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(dk_out, c->io[8].p, bq, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(dv_out, c->io[10].p, bv, cudaMemcpyDeviceToHost, st));
+    if (dbias && E) CUDA_TRY(cudaMemcpyAsync(dbias, dbias_dev, E * as, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+  }
+  bias_buf.release();
+  return rc;
+}
+
+int gte_sparse_attn_fwd_bwd_host(gte_ctx* c, const gte_plan* plan, int dtype, int H, int dk, int dv,
+                                 const void* q, const void* k, const void* v, const void* dout,
+                                 const void* bias, void* out, void* dq, void* dk_out, void* dv_out,
+                                 void* dbias) {
+  int rc = check_attn_args(plan, dtype, H, dk, dv, (int64_t)H * dk, (int64_t)H * dv);
+  if (rc) return rc;
+  const size_t S = (size_t)plan->rows, E = (size_t)plan->nnz, es = elem_size(dtype), as = acc_size(dtype);
+  const size_t bq = S * H * dk * es, bv = S * H * dv * es;
+  cudaStream_t st = c->stream;
+  for (int i : {0, 1, 7, 8}) CUDA_TRY(c->io[i].ensure(bq));
+  for (int i : {2, 3, 9, 10}) CUDA_TRY(c->io[i].ensure(bv));
+  CUDA_TRY(c->io[4].ensure(S * H * as));
+  CUDA_TRY(c->io[5].ensure((E + 1) * as));
+  CUDA_TRY(c->io[6].ensure((E + 1) * as));
+  CUDA_TRY(cudaMemcpyAsync(c->io[0].p, q, bq, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(c->io[1].p, k, bq, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(c->io[2].p, v, bv, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(c->io[9].p, dout, bv, cudaMemcpyHostToDevice, st));
+  if (bias) CUDA_TRY(cudaMemcpyAsync(c->io[6].p, bias, E * as, cudaMemcpyHostToDevice, st));
+  const void* bias_dev = bias ? c->io[6].p : nullptr;
+  rc = gte_sparse_attn_fwd(c, plan, dtype, H, dk, dv, c->io[0].p, c->io[1].p, (int64_t)H * dk, c->io[2].p,
+                           (int64_t)H * dv, bias_dev, nullptr, c->io[3].p, c->io[4].p, 0);
+  if (rc) return rc;
+  rc = gte_sparse_attn_bwd(c, plan, dtype, H, dk, dv, c->io[0].p, c->io[1].p, (int64_t)H * dk, c->io[2].p,
+                           (int64_t)H * dv, c->io[3].p, c->io[4].p, c->io[9].p, bias_dev, nullptr,
+                           c->io[7].p, c->io[8].p, c->io[10].p, c->io[5].p);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(out, c->io[3].p, bv, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(dq, c->io[7].p, bq, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(dk_out, c->io[8].p, bq, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(dv_out, c->io[10].p, bv, cudaMemcpyDeviceToHost, st));
+  if (dbias && E) CUDA_TRY(cudaMemcpyAsync(dbias, c->io[5].p, E * as, cudaMemcpyDeviceToHost, st));
+  return drain_errors(c);
+}
+
+}  // extern "C"
+
+namespace gte_b200 {
+cudaError_t launch_finite_rows(int dtype, const void* k, const void* v, const int32_t* rows, int nrows,
+                               int64_t ldq, int64_t ldv, int64_t wq, int64_t wv, int* err, cudaStream_t st) {
+  const unsigned grid = nrows < 4096 ? (unsigned)nrows : 4096u;
+  switch (dtype) {
+    case GTE_F64:
+      finite_rows_kernel<double><<<grid, 64, 0, st>>>((const double*)k, (const double*)v, rows, nrows, ldq, ldv, wq, wv, err);
+      break;
+    case GTE_F32:
+      finite_rows_kernel<float><<<grid, 64, 0, st>>>((const float*)k, (const float*)v, rows, nrows, ldq, ldv, wq, wv, err);
+      break;
+    default:
+      finite_rows_kernel<__nv_bfloat16><<<grid, 64, 0, st>>>((const __nv_bfloat16*)k, (const __nv_bfloat16*)v, rows,
+                                                              nrows, ldq, ldv, wq, wv, err);
+  }
+  return cudaGetLastError();
+}
+}  // namespace gte_b200

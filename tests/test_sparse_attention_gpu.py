@@ -1,0 +1,216 @@
+"""Parity of the sm_100a sparse graph-attention kernels (through the C ABI)
+against the CPU oracle (oracle/liboracle.so, itself pinned to the compiled
+reference by tests/test_oracle_golden.py).
+
+Tolerances (BASELINE.md "Parity definition"), per tensor:
+  f64: max|a-b| <= 1e-12*max|ref|
+  f32: max|a-b| <= 1e-5*max|ref|  and  ||a-b||/||ref|| <= 1e-5
+  bf16 (inputs rounded to bf16, fp32 accumulate, bf16 outputs):
+       max|a-b| <= 2e-2*max|ref|  and  ||a-b||/||ref|| <= 1e-2
+The oracle always runs in fp64 on the *same* (dtype-rounded) inputs.
+"""
+import numpy as np
+import pytest
+
+from conftest import rel_err
+from oracle import CSR
+
+from paper_2407_14106_b200 import attention as A
+from paper_2407_14106_b200._lib import ConfigError, DataError
+from paper_2407_14106_b200.datagen import c1_edges, community_graph, csr_from_pairs
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"f64": (1e-12, 1e-12), "f32": (1e-5, 1e-5), "bf16": (2e-2, 1e-2)}
+
+
+def assert_close(got, want, dtype, what=""):
+    e_max, e_nrm = rel_err(got, want)
+    tmax, tnrm = TOL[dtype]
+    assert e_max <= tmax and e_nrm <= tnrm, f"{what} [{dtype}] max-norm {e_max:.3g} l2 {e_nrm:.3g}"
+
+
+def pat_of(g: CSR) -> A.AttnPattern:
+    return A.AttnPattern(g.n, g.row_off, g.cols)
+
+
+# ---------------------------------------------------------------- golden, reference-shaped API
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_golden_cases_per_head(cuda, golden, orc, dtype):
+    d = golden("attention_small.npz")
+    for ci in range(int(d["ncases"])):
+        p = f"a{ci}_"
+        g = CSR(int(d[p + "g_n"]), d[p + "g_ro"], d[p + "g_cols"])
+        bias = d[p + "bias"] if p + "bias" in d else None
+        wm = d[p + "wm"] if p + "wm" in d else None
+        q, k, v, up = (d[p + n] for n in ("q", "k", "v", "up"))
+        if dtype == "f32":  # oracle on the fp32-rounded inputs
+            q, k, v, up = (x.astype(np.float32).astype(np.float64) for x in (q, k, v, up))
+            bias = None if bias is None else bias.astype(np.float32).astype(np.float64)
+            want = orc.sparse_fwd(q, k, v, g, bias, wm)
+            wq, wk, wv, wb = orc.sparse_bwd(q, k, v, g, bias, wm, up)
+        else:
+            want = d[p + "out"]
+            wq, wk, wv, wb = (d[p + n] for n in ("dq", "dk", "dv", "db"))
+        res = A.sparse_attention(q, k, v, pat_of(g), bias, wm, dtype=dtype)
+        assert_close(res.output, want, dtype, f"case {ci} out")
+        assert res.macs.score_macs == g.nnz * q.shape[1]
+        gr = A.sparse_attention_backward(q, k, v, pat_of(g), bias, wm, up, dtype=dtype)
+        for got, w, nm in ((gr.dq, wq, "dq"), (gr.dk, wk, "dk"), (gr.dv, wv, "dv"), (gr.dbias, wb, "dbias")):
+            assert_close(got, w, dtype, f"case {ci} {nm}")
+
+
+# ---------------------------------------------------------------- multi-head device path
+
+def _torch_dtype(dtype):
+    import torch
+
+    return {"f64": torch.float64, "f32": torch.float32, "bf16": torch.bfloat16}[dtype]
+
+
+def run_device(row_off, cols, H, dh, dtype, seed=0, with_bias=True, with_wm=False, S=None):
+    """Runs fwd+bwd through DeviceSparseAttention; returns the dtype-rounded fp64
+    inputs and the outputs, as numpy fp64."""
+    import torch
+
+    S = row_off.shape[0] - 1
+    E = cols.shape[0]
+    rng = np.random.default_rng(seed)
+    td = _torch_dtype(dtype)
+    acc = torch.float64 if dtype == "f64" else torch.float32
+    dev = torch.device("cuda:0")
+    q, k, v, do = (torch.tensor(rng.standard_normal((S, H * dh)), dtype=td, device=dev) for _ in range(4))
+    bias = torch.tensor(rng.normal(0, 0.3, E), dtype=acc, device=dev) if with_bias else None
+    wm = torch.tensor((rng.random((H, E)) < 0.7) / 0.7, dtype=acc, device=dev) if with_wm else None
+    plan = A.DevicePlan.from_host(row_off, cols)
+    att = A.DeviceSparseAttention(plan, H, dh, dh, dtype)
+    out, lse = att.forward(q, k, v, bias, wm)
+    dq, dk, dv, db = att.backward(q, k, v, out, lse, do, bias, wm)
+    plan.ctx.sync()
+    f = lambda t: None if t is None else t.double().cpu().numpy()  # noqa: E731
+    return dict(q=f(q), k=f(k), v=f(v), do=f(do), bias=f(bias), wm=f(wm), out=f(out), dq=f(dq), dk=f(dk), dv=f(dv),
+                db=f(db)[:E], lse=f(lse))
+
+
+def oracle_multihead(orc, g: CSR, r, H, dh):
+    S = g.n
+    out = np.zeros((S, H * dh))
+    dq, dk, dv = np.zeros_like(out), np.zeros_like(out), np.zeros_like(out)
+    db = np.zeros(g.nnz)
+    for h in range(H):
+        sl = slice(h * dh, (h + 1) * dh)
+        wm = None if r["wm"] is None else r["wm"][h]
+        out[:, sl] = orc.sparse_fwd(r["q"][:, sl], r["k"][:, sl], r["v"][:, sl], g, r["bias"], wm)
+        a, b, c, e = orc.sparse_bwd(r["q"][:, sl], r["k"][:, sl], r["v"][:, sl], g, r["bias"], wm, r["do"][:, sl])
+        dq[:, sl], dk[:, sl], dv[:, sl] = a, b, c
+        db += e  # head order 0..H-1 as parallel.cpp:319
+    return out, dq, dk, dv, db
+
+
+@pytest.fixture(scope="module")
+def c1_graph():
+    s, t = c1_edges()
+    ro, co = csr_from_pairs(4096, s, t)
+    return CSR(4096, ro, co)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16", "f64"])
+def test_c1_multihead(cuda, orc, c1_graph, dtype):
+    g = c1_graph
+    assert g.nnz == 69497
+    r = run_device(g.row_off, g.cols, 8, 8, dtype, seed=1)
+    want = oracle_multihead(orc, g, r, 8, 8)
+    for got, w, nm in zip((r["out"], r["dq"], r["dk"], r["dv"], r["db"]), want, ("out", "dq", "dk", "dv", "dbias")):
+        assert_close(got, w, dtype, f"C1 {nm}")
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_c1_with_dropout_mask(cuda, orc, c1_graph, dtype):
+    r = run_device(c1_graph.row_off, c1_graph.cols, 8, 8, dtype, seed=2, with_wm=True)
+    want = oracle_multihead(orc, c1_graph, r, 8, 8)
+    for got, w, nm in zip((r["out"], r["dq"], r["dk"], r["dv"], r["db"]), want, ("out", "dq", "dk", "dv", "dbias")):
+        assert_close(got, w, dtype, f"C1+mask {nm}")
+
+
+@pytest.mark.parametrize("H,dh", [(1, 8), (2, 16), (4, 4), (3, 5), (16, 8), (32, 24), (8, 64)])
+def test_head_geometries_f32(cuda, orc, H, dh):
+    ro, co = community_graph(1500, 9.0, community=64, seed=H * 100 + dh)
+    g = CSR(1500, ro, co)
+    r = run_device(ro, co, H, dh, "f32", seed=H + dh)
+    want = oracle_multihead(orc, g, r, H, dh)
+    for got, w, nm in zip((r["out"], r["dq"], r["dk"], r["dv"], r["db"]), want, ("out", "dq", "dk", "dv", "dbias")):
+        assert_close(got, w, "f32", f"H={H} dh={dh} {nm}")
+
+
+def test_hub_rows_and_columns_f32(cuda, orc):
+    # a global token attending / attended by every node (proj/src/model.cpp:349-357)
+    n = 5000
+    s, t = c1_edges(n - 1, 6, 9)
+    glob = n - 1
+    src = np.r_[s, np.arange(n - 1), np.full(n - 1, glob)]
+    dst = np.r_[t, np.full(n - 1, glob), np.arange(n - 1)]
+    ro, co = csr_from_pairs(n, src, dst)
+    g = CSR(n, ro, co)
+    r = run_device(ro, co, 8, 8, "f32", seed=5)
+    want = oracle_multihead(orc, g, r, 8, 8)
+    for got, w, nm in zip((r["out"], r["dq"], r["dk"], r["dv"], r["db"]), want, ("out", "dq", "dk", "dv", "dbias")):
+        assert_close(got, w, "f32", f"hub {nm}")
+
+
+# ---------------------------------------------------------------- edge semantics
+
+def test_empty_and_singleton_rows_exact(cuda):
+    # row 0 -> {1}; row 1 -> {} ; row 2 -> {0,1,2}; row 3 -> {3}
+    ro = np.array([0, 1, 1, 4, 5], dtype=np.int64)
+    co = np.array([1, 0, 1, 2, 3], dtype=np.int64)
+    pat = A.AttnPattern(4, ro, co)
+    rng = np.random.default_rng(0)
+    q, k, v, up = (rng.standard_normal((4, 3)) for _ in range(4))
+    wm = np.array([2.0, 1.0, 0.0, 1.5, 0.5])
+    for dtype in ("f64", "f32"):
+        res = A.sparse_attention(q, k, v, pat, None, wm, dtype=dtype)
+        vv = v.astype(np.float32) if dtype == "f32" else v
+        assert np.array_equal(res.output[0], (2.0 * vv[1]).astype(res.output.dtype))  # deg 1: m * v_j exactly
+        assert np.all(res.output[1] == 0)  # deg 0: zero row
+        assert np.array_equal(res.output[3], (0.5 * vv[3]).astype(res.output.dtype))
+        gr = A.sparse_attention_backward(q, k, v, pat, None, wm, up, dtype=dtype)
+        assert np.all(gr.dq[0] == 0) and np.all(gr.dq[1] == 0) and np.all(gr.dq[3] == 0)
+        assert gr.dbias[0] == 0 and gr.dbias[4] == 0
+    with pytest.raises(DataError, match=r"row 1 attends to nothing; run add_self_loops"):
+        A.edge_sparse_attention(q, k, v, A.Graph(4, ro, co))
+
+
+def test_non_finite_inputs_raise(cuda):
+    ro = np.array([0, 1, 2, 3], dtype=np.int64)
+    co = np.array([0, 1, 1], dtype=np.int64)  # row 2 never referenced as a column
+    pat = A.AttnPattern(3, ro, co)
+    base = np.ones((3, 2))
+    for which, name in ((0, "Q"), (1, "K"), (2, "V")):
+        args = [base.copy(), base.copy(), base.copy()]
+        args[which][2, 1] = np.inf if which != 1 else np.nan
+        with pytest.raises(DataError, match=f"non-finite {name}"):
+            A.sparse_attention(*args, pat)
+    ok = A.sparse_attention(base, base, base, pat)
+    assert np.allclose(ok.output, 1.0)
+
+
+def test_shape_errors(cuda):
+    pat = A.AttnPattern(2, np.array([0, 1, 2]), np.array([0, 1]))
+    with pytest.raises(ConfigError, match="row counts differ"):
+        A.sparse_attention(np.zeros((2, 2)), np.zeros((3, 2)), np.zeros((2, 2)), pat)
+    with pytest.raises(ConfigError, match="bias must cover"):
+        A.sparse_attention(np.zeros((2, 2)), np.zeros((2, 2)), np.zeros((2, 2)), pat, bias=np.zeros(3))
+    with pytest.raises(ConfigError, match="pattern/sequence length mismatch"):
+        A.sparse_attention(np.zeros((3, 2)), np.zeros((3, 2)), np.zeros((3, 2)), pat)
+
+
+def test_complete_graph_equals_dense(cuda, orc):
+    # reference proj/tests/test_attention.cpp:75-87 / acceptance C1
+    rng = np.random.default_rng(100)
+    for s in (4, 7, 10, 13, 16):
+        ro, co = csr_from_pairs(s, np.repeat(np.arange(s), s), np.tile(np.arange(s), s), self_loops=False)
+        q, k, v = (rng.standard_normal((s, 4)) for _ in range(3))
+        dense = orc.dense_fwd(q, k, v)
+        got = A.edge_sparse_attention(q, k, v, A.Graph(s, ro, co)).output
+        assert np.abs(got - dense).max() <= 1e-12
