@@ -264,12 +264,13 @@ def _forward_nocheck(q, k, v, plan, bias, wm, dtype):
     S, dk = q.shape
     dv = v.shape[1]
     qq, kk, vv = _prep(q, dt), _prep(k, dt), _prep(v, dt)
+    b, w = _prep(bias, dt), _prep(wm, dt)  # keep the converted copies alive across the call
     out = np.zeros((S, dv), dt)
     lse = np.zeros((S, 1), dt)
     if S > 0:
         rc = _lib.lib().gte_sparse_attn_fwd_host(plan.ctx.h, plan.h, _lib.DTYPES[dtype], 1, dk, dv, qq.ctypes.data,
-                                                 kk.ctypes.data, vv.ctypes.data, _ptr(_prep(bias, dt)),
-                                                 _ptr(_prep(wm, dt)), out.ctypes.data, lse.ctypes.data, 0)
+                                                 kk.ctypes.data, vv.ctypes.data, _ptr(b), _ptr(w),
+                                                 out.ctypes.data, lse.ctypes.data, 0)
         if rc == _lib.GTE_DATA:
             # the reference backward performs no finiteness check
             # (attention.cpp:241-320); NaNs simply propagate
