@@ -104,6 +104,53 @@ int gte_sparse_attn_fwd_bwd_host(gte_ctx* ctx, const gte_plan* plan, int dtype, 
                                  const void* dout, const void* bias, void* out, void* dq,
                                  void* dk_out, void* dv_out, void* dbias);
 
+/* ---- graph builders (device int32 CSR, bit-exact with the reference) ----
+ * graph_from_edges   proj/src/graph.cpp:49-66  (range check -> DataError, sort, unique)
+ * add_self_loops     proj/src/graph.cpp:127-149
+ * permute_graph      proj/src/partition.cpp:435-456 (forward: host int64 old->new)
+ * Output buffers: d_cols capacity m (graph_from_edges), nnz + n (add_self_loops),
+ * nnz (permute_graph); row pointers n + 1. */
+int gte_graph_from_edges(gte_ctx* ctx, int64_t n, int64_t m, const int32_t* d_src, const int32_t* d_dst,
+                         int32_t* d_row_ptr, int32_t* d_cols, int64_t* nnz_out);
+int gte_add_self_loops(gte_ctx* ctx, int64_t n, int64_t nnz, const int32_t* d_row_ptr, const int32_t* d_cols,
+                       int32_t* d_out_row_ptr, int32_t* d_out_cols, int64_t* nnz_out);
+int gte_permute_graph(gte_ctx* ctx, int64_t n, int64_t nnz, const int32_t* d_row_ptr, const int32_t* d_cols,
+                      const int64_t* forward, int32_t* d_out_row_ptr, int32_t* d_out_cols);
+
+/* ---- cluster-aware order (reference proj/src/partition.cpp) ----
+ * gte_reorder: host CSR (int64, the reference Graph layout) -> Permutation;
+ * bit-identical to gte::reorder(g, k, seed) (partition.cpp:413-433). Host-side
+ * greedy (matching/FM/growth are sequential); see csrc/reorder.cpp. */
+int gte_reorder(int64_t n, int64_t nnz, const int64_t* row_off, const int64_t* cols, int64_t k, uint64_t seed,
+                int64_t* forward, int64_t* inverse);
+int gte_cluster_boundaries(int64_t n, int64_t k, int64_t* boundaries);
+/* k x k cell histogram on the GPU; forward NULL = graph already in cluster
+ * order. Outputs host arrays bnd[k+1], cell_nnz[k*k], cell_density[k*k]
+ * (fp64, bit-exact: partition.cpp:514-539). */
+int gte_build_cluster_grid(gte_ctx* ctx, int64_t n, int64_t nnz, const int32_t* d_row_ptr, const int32_t* d_cols,
+                           const int64_t* forward, int64_t k, int64_t* bnd, int64_t* cell_nnz,
+                           double* cell_density);
+int gte_diagonal_edge_fraction(int64_t k, const int64_t* cell_nnz, double* out);
+
+/* ---- Elastic Computation Reformation (reference proj/src/reformation.cpp) ----
+ * gte_pack_subblocks: reformation.cpp:56-109, same tile sequence; tiles_rc
+ * capacity 2*ceil(m/d_b^2).
+ * gte_build_layout: reformation.cpp:111-195. g_perm (device CSR) must be in the
+ * grid's cluster order. strategy 0 = Indolent (threshold beta_g), 1 = Elastic
+ * (threshold beta_thre); Transferred iff cell_density < threshold (fp64). */
+typedef struct gte_layout gte_layout;
+int gte_pack_subblocks(int64_t m, const int64_t* er, const int64_t* ec, int64_t n_rows, int64_t n_cols,
+                       int64_t d_b, int64_t* tiles_rc, int64_t* ntiles);
+int gte_build_layout(gte_ctx* ctx, int64_t n, int64_t nnz, const int32_t* d_row_ptr, const int32_t* d_cols,
+                     int64_t k, const int64_t* bnd, const int64_t* cell_nnz, const double* cell_density,
+                     int strategy, double beta_thre, double beta_g, int64_t d_b, gte_layout** out);
+int gte_layout_info(const gte_layout* L, int64_t* transferred_cells, int64_t* n_blocks, int64_t* dropped_edges,
+                    int64_t* pattern_nnz);
+int gte_layout_cells(const gte_layout* L, int32_t* cell_state, int64_t* block_off, int64_t* blocks);
+int gte_layout_pattern_device(const gte_layout* L, const int32_t** d_row_ptr, const int32_t** d_cols);
+int gte_layout_pattern_host(const gte_layout* L, int64_t* row_off, int64_t* cols);
+int gte_layout_destroy(gte_layout* L);
+
 #ifdef __cplusplus
 }
 #endif

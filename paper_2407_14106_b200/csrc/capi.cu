@@ -2,6 +2,8 @@
 // device pattern plans (CSR + CSC built on the GPU with radix sort/scan), and
 // the sparse attention entries with their host-pointer twins.
 #include <climits>
+#include <cstdlib>
+#include <initializer_list>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -10,7 +12,7 @@
 #include <cub/cub.cuh>
 
 #include "../../include/gte_b200.h"
-#include "attn_launch.cuh"
+#include "fast_launch.cuh"
 
 using namespace gte_b200;
 
@@ -229,6 +231,33 @@ int pick_lpn(int H) {
   return l;
 }
 
+// Fast (memory-level-parallel) family: f32/bf16, dk == dv, head chunk a
+// power-of-two number of 16-byte pieces, all heads of a neighbour within one
+// warp, 16-byte aligned rows. Returns lanes-per-head, or 0 if not eligible.
+int fast_lph(int dtype, int H, int dk, int dv, int64_t ldq, int64_t ldv, std::initializer_list<const void*> ptrs) {
+  static const bool disabled = getenv("GTE_DISABLE_FAST") != nullptr;
+  if (disabled) return 0;
+  if (dtype != GTE_F32 && dtype != GTE_BF16) return 0;
+  if (dk != dv) return 0;
+  const int64_t es = (int64_t)elem_size(dtype);
+  if ((dk * es) % 16 != 0 || (ldq * es) % 16 != 0 || (ldv * es) % 16 != 0) return 0;
+  const int lph = (int)(dk * es / 16);
+  if (lph != 1 && lph != 2 && lph != 4 && lph != 8) return 0;
+  int lpn = 1;
+  while (lpn < H) lpn <<= 1;
+  if (lpn * lph > 32) return 0;
+  for (const void* q : ptrs)
+    if (q && (reinterpret_cast<uintptr_t>(q) & 15)) return 0;
+  return lph;
+}
+
+cudaError_t dispatch_fast(int dtype, int which, const SparseArgs& a, int lph, cudaStream_t st) {
+  int lpn = 1;
+  while (lpn < a.H) lpn <<= 1;
+  lpn *= lph;
+  return dtype == GTE_F32 ? launch_fast_f32(which, a, lph, lpn, st) : launch_fast_bf16(which, a, lph, lpn, st);
+}
+
 cudaError_t dispatch(int dtype, int which, const SparseArgs& a, int dht, int lpn, cudaStream_t st) {
   switch (dtype) {
     case GTE_F64: return launch_sparse_f64(which, a, dht, lpn, st);
@@ -401,7 +430,11 @@ int gte_sparse_attn_fwd(gte_ctx* c, const gte_plan* plan, int dtype, int H, int 
   a.vec_qk = dk == dht && (ldq * es) % 16 == 0 && aligned16(q) && aligned16(k);
   a.vec_v = dv == dht && (ldv * es) % 16 == 0 && aligned16(v) && aligned16(out);
   if (plan->rows == 0) return GTE_OK;
-  CUDA_TRY(dispatch(dtype, kFwd, a, dht, lpn, c->stream));
+  const int lph = fast_lph(dtype, H, dk, dv, ldq, ldv, {q, k, v, out});
+  if (lph)
+    CUDA_TRY(dispatch_fast(dtype, kFwd, a, lph, c->stream));
+  else
+    CUDA_TRY(dispatch(dtype, kFwd, a, dht, lpn, c->stream));
   c->launches += 1;
   if (plan->n_unref > 0) {
     CUDA_TRY(launch_finite_rows(dtype, k, v, plan->unref, (int)plan->n_unref, ldq, ldv, (int64_t)H * dk,
@@ -439,8 +472,14 @@ int gte_sparse_attn_bwd(gte_ctx* c, const gte_plan* plan, int dtype, int H, int 
   const size_t es = elem_size(dtype);
   a.vec_qk = dk == dht && (ldq * es) % 16 == 0 && aligned16(q) && aligned16(k) && aligned16(dq) && aligned16(dk_out);
   a.vec_v = dv == dht && (ldv * es) % 16 == 0 && aligned16(v) && aligned16(out) && aligned16(dout) && aligned16(dv_out);
-  CUDA_TRY(dispatch(dtype, kBwdRows, a, dht, lpn, c->stream));
-  CUDA_TRY(dispatch(dtype, kBwdCols, a, dht, lpn, c->stream));
+  const int lph = fast_lph(dtype, H, dk, dv, ldq, ldv, {q, k, v, out, dout, dq, dk_out, dv_out});
+  if (lph) {
+    CUDA_TRY(dispatch_fast(dtype, kBwdRows, a, lph, c->stream));
+    CUDA_TRY(dispatch_fast(dtype, kBwdCols, a, lph, c->stream));
+  } else {
+    CUDA_TRY(dispatch(dtype, kBwdRows, a, dht, lpn, c->stream));
+    CUDA_TRY(dispatch(dtype, kBwdCols, a, dht, lpn, c->stream));
+  }
   c->launches += 2;
   return GTE_OK;
 }
@@ -558,6 +597,10 @@ int gte_sparse_attn_fwd_bwd_host(gte_ctx* c, const gte_plan* plan, int dtype, in
 }  // extern "C"
 
 namespace gte_b200 {
+int set_error(int code, const std::string& msg) { return fail(code, msg); }
+int64_t& ctx_launch_counter(gte_ctx* c) { return c->launches; }
+void* ctx_stream(gte_ctx* c) { return (void*)c->stream; }
+
 cudaError_t launch_finite_rows(int dtype, const void* k, const void* v, const int32_t* rows, int nrows,
                                int64_t ldq, int64_t ldv, int64_t wq, int64_t wv, int* err, cudaStream_t st) {
   const unsigned grid = nrows < 4096 ? (unsigned)nrows : 4096u;

@@ -1,0 +1,56 @@
+// Dispatch for the memory-level-parallel kernels (attn_fast.cuh).
+#pragma once
+
+#include "attn_fast.cuh"
+#include "attn_launch.cuh"
+
+namespace gte_b200 {
+
+#ifndef GTE_FAST_EPL
+#define GTE_FAST_EPL 8
+#endif
+
+template <typename T, int LPH, int LPN>
+cudaError_t launch_fast_one(int which, const SparseArgs& a, cudaStream_t st) {
+  constexpr int kBlock = 256;
+  constexpr int EPL = GTE_FAST_EPL;
+  int64_t grid = (a.S * 32 + kBlock - 1) / kBlock;
+  if (grid > (1LL << 30)) grid = 1LL << 30;
+  if (grid < 1) grid = 1;
+  switch (which) {
+    case kFwd: fast_fwd_kernel<T, LPH, LPN, EPL><<<(unsigned)grid, kBlock, 0, st>>>(a); break;
+    case kBwdRows: fast_bwd_rows_kernel<T, LPH, LPN, EPL><<<(unsigned)grid, kBlock, 0, st>>>(a); break;
+    default: fast_bwd_cols_kernel<T, LPH, LPN, EPL><<<(unsigned)grid, kBlock, 0, st>>>(a); break;
+  }
+  return cudaGetLastError();
+}
+
+template <typename T, int LPH>
+cudaError_t launch_fast_lpn(int which, const SparseArgs& a, int lpn, cudaStream_t st) {
+  switch (lpn) {
+    case 1: if constexpr (LPH <= 1) return launch_fast_one<T, LPH, 1>(which, a, st); break;
+    case 2: if constexpr (LPH <= 2) return launch_fast_one<T, LPH, 2>(which, a, st); break;
+    case 4: if constexpr (LPH <= 4) return launch_fast_one<T, LPH, 4>(which, a, st); break;
+    case 8: if constexpr (LPH <= 8) return launch_fast_one<T, LPH, 8>(which, a, st); break;
+    case 16: return launch_fast_one<T, LPH, 16>(which, a, st);
+    case 32: return launch_fast_one<T, LPH, 32>(which, a, st);
+    default: break;
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <typename T>
+cudaError_t launch_fast_t(int which, const SparseArgs& a, int lph, int lpn, cudaStream_t st) {
+  switch (lph) {
+    case 1: return launch_fast_lpn<T, 1>(which, a, lpn, st);
+    case 2: return launch_fast_lpn<T, 2>(which, a, lpn, st);
+    case 4: return launch_fast_lpn<T, 4>(which, a, lpn, st);
+    case 8: return launch_fast_lpn<T, 8>(which, a, lpn, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_fast_f32(int which, const SparseArgs& a, int lph, int lpn, cudaStream_t st);
+cudaError_t launch_fast_bf16(int which, const SparseArgs& a, int lph, int lpn, cudaStream_t st);
+
+}  // namespace gte_b200
