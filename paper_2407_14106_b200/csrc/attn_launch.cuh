@@ -3,23 +3,39 @@
 // attn_f64.cu) so nvcc builds them in parallel.
 #pragma once
 
+#include <cstdlib>
+
 #include "attn_sparse.cuh"
 
 namespace gte_b200 {
 
 enum SparseKernel { kFwd = 0, kBwdRows = 1, kBwdCols = 2 };
 
+// Rows (resp. columns) per CTA: a contiguous range per CTA so a cluster-ordered
+// sequence's gathers stay L1-resident; GTE_ROWS_PER_CTA overrides (tuning).
+inline int64_t rows_per_cta_for(int64_t S) {
+  static const int64_t env = [] {
+    const char* e = getenv("GTE_ROWS_PER_CTA");
+    return e ? atoll(e) : 0LL;
+  }();
+  int64_t r = env > 0 ? env : 128;
+  // keep at least ~4 CTAs per SM for balance on short sequences
+  while (r > 8 && (S + r - 1) / r < 148 * 4) r >>= 1;
+  return r < 8 ? 8 : r;
+}
+
 template <typename T, int DHT, int LPN>
 cudaError_t launch_one(int which, const SparseArgs& a, cudaStream_t st) {
   constexpr int kBlock = 256;
-  const int64_t warps = a.S;
-  int64_t grid = (warps * 32 + kBlock - 1) / kBlock;
+  SparseArgs b = a;
+  b.rows_per_cta = rows_per_cta_for(a.S);
+  int64_t grid = (a.S + b.rows_per_cta - 1) / b.rows_per_cta;
   if (grid > (1LL << 30)) grid = 1LL << 30;
   if (grid < 1) grid = 1;
   switch (which) {
-    case kFwd: sparse_fwd_kernel<T, DHT, LPN><<<(unsigned)grid, kBlock, 0, st>>>(a); break;
-    case kBwdRows: sparse_bwd_rows_kernel<T, DHT, LPN><<<(unsigned)grid, kBlock, 0, st>>>(a); break;
-    default: sparse_bwd_cols_kernel<T, DHT, LPN><<<(unsigned)grid, kBlock, 0, st>>>(a); break;
+    case kFwd: sparse_fwd_kernel<T, DHT, LPN><<<(unsigned)grid, kBlock, 0, st>>>(b); break;
+    case kBwdRows: sparse_bwd_rows_kernel<T, DHT, LPN><<<(unsigned)grid, kBlock, 0, st>>>(b); break;
+    default: sparse_bwd_cols_kernel<T, DHT, LPN><<<(unsigned)grid, kBlock, 0, st>>>(b); break;
   }
   return cudaGetLastError();
 }

@@ -56,7 +56,21 @@ struct SparseArgs {
   int forbid_empty = 0;
   int vec_qk = 0, vec_v = 0;
   int* err = nullptr;  // [0] non-finite flag, [1] first empty row (atomicMin)
+  // Each CTA owns a contiguous range of rows (columns for the CSC pass); its
+  // warps stride through it. Contiguous ranges keep a cluster-ordered
+  // sequence's neighbour rows hot in that SM's L1.
+  int64_t rows_per_cta = 8;
 };
+
+struct WarpRange {
+  int64_t first, last, step;
+};
+
+__device__ __forceinline__ WarpRange warp_range(const SparseArgs& p) {
+  const int64_t r0 = (int64_t)blockIdx.x * p.rows_per_cta;
+  const int64_t r1 = r0 + p.rows_per_cta < p.S ? r0 + p.rows_per_cta : p.S;
+  return {r0 + (threadIdx.x >> 5), r1, (int64_t)(blockDim.x >> 5)};
+}
 
 // Edges per lane per chunk: up to LPN (one full warp of neighbours per chunk),
 // at most 8, and bounded so the unrolled gathers keep <= budget/DHT rows live.
@@ -101,10 +115,10 @@ __global__ void __launch_bounds__(256) sparse_fwd_kernel(SparseArgs p) {
   A* __restrict__ LSE = static_cast<A*>(p.lse);
   const bool vqk = p.vec_qk, vv = p.vec_v;
   const int64_t qoff = (int64_t)hl * p.dk, voff = (int64_t)hl * p.dv;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const WarpRange wr = warp_range(p);
   int bad = 0;  // bit 0: Q, bit 1: K, bit 2: V non-finite
 
-  for (int64_t i = (((int64_t)blockIdx.x * blockDim.x) + threadIdx.x) >> 5; i < p.S; i += nwarps) {
+  for (int64_t i = wr.first; i < wr.last; i += wr.step) {
     const int beg = __ldg(p.row_ptr + i), end = __ldg(p.row_ptr + i + 1);
     A q[DHT], acc[DHT];
 #pragma unroll
@@ -227,9 +241,9 @@ __global__ void __launch_bounds__(256) sparse_bwd_rows_kernel(SparseArgs p) {
   A* __restrict__ DB = static_cast<A*>(p.dbias);
   const bool vqk = p.vec_qk, vv = p.vec_v;
   const int64_t qoff = (int64_t)hl * p.dk, voff = (int64_t)hl * p.dv;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const WarpRange wr = warp_range(p);
 
-  for (int64_t i = (((int64_t)blockIdx.x * blockDim.x) + threadIdx.x) >> 5; i < p.S; i += nwarps) {
+  for (int64_t i = wr.first; i < wr.last; i += wr.step) {
     const int beg = __ldg(p.row_ptr + i), end = __ldg(p.row_ptr + i + 1);
     A dq[DHT];
 #pragma unroll
@@ -330,9 +344,9 @@ __global__ void __launch_bounds__(256) sparse_bwd_cols_kernel(SparseArgs p) {
   T* __restrict__ DV = static_cast<T*>(p.dv_out);
   const bool vqk = p.vec_qk, vv = p.vec_v;
   const int64_t qoff = (int64_t)hl * p.dk, voff = (int64_t)hl * p.dv;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const WarpRange wr = warp_range(p);
 
-  for (int64_t j = (((int64_t)blockIdx.x * blockDim.x) + threadIdx.x) >> 5; j < p.S; j += nwarps) {
+  for (int64_t j = wr.first; j < wr.last; j += wr.step) {
     const int beg = __ldg(p.col_ptr + j), end = __ldg(p.col_ptr + j + 1);
     A kr[DHT], vr[DHT], gk[DHT], gv[DHT];
 #pragma unroll

@@ -234,9 +234,12 @@ int pick_lpn(int H) {
 // Fast (memory-level-parallel) family: f32/bf16, dk == dv, head chunk a
 // power-of-two number of 16-byte pieces, all heads of a neighbour within one
 // warp, 16-byte aligned rows. Returns lanes-per-head, or 0 if not eligible.
-int fast_lph(int dtype, int H, int dk, int dv, int64_t ldq, int64_t ldv, std::initializer_list<const void*> ptrs) {
+int fast_lph(int dtype, int64_t S, int H, int dk, int dv, int64_t ldq, int64_t ldv,
+             std::initializer_list<const void*> ptrs) {
   static const bool disabled = getenv("GTE_DISABLE_FAST") != nullptr;
   if (disabled) return 0;
+  // 32-bit gather offsets inside the kernels
+  if ((S + 1) * (ldq > ldv ? ldq : ldv) * (int64_t)elem_size(dtype) >= (int64_t(1) << 32)) return 0;
   if (dtype != GTE_F32 && dtype != GTE_BF16) return 0;
   if (dk != dv) return 0;
   const int64_t es = (int64_t)elem_size(dtype);
@@ -430,13 +433,13 @@ int gte_sparse_attn_fwd(gte_ctx* c, const gte_plan* plan, int dtype, int H, int 
   a.vec_qk = dk == dht && (ldq * es) % 16 == 0 && aligned16(q) && aligned16(k);
   a.vec_v = dv == dht && (ldv * es) % 16 == 0 && aligned16(v) && aligned16(out);
   if (plan->rows == 0) return GTE_OK;
-  const int lph = fast_lph(dtype, H, dk, dv, ldq, ldv, {q, k, v, out});
+  const int lph = fast_lph(dtype, plan->rows, H, dk, dv, ldq, ldv, {q, k, v, out});
   if (lph)
     CUDA_TRY(dispatch_fast(dtype, kFwd, a, lph, c->stream));
   else
     CUDA_TRY(dispatch(dtype, kFwd, a, dht, lpn, c->stream));
   c->launches += 1;
-  if (plan->n_unref > 0) {
+  if (!lph && plan->n_unref > 0) {  // the fast kernels check every row's own K/V
     CUDA_TRY(launch_finite_rows(dtype, k, v, plan->unref, (int)plan->n_unref, ldq, ldv, (int64_t)H * dk,
                                 (int64_t)H * dv, c->d_err, c->stream));
     c->launches += 1;
@@ -472,7 +475,7 @@ int gte_sparse_attn_bwd(gte_ctx* c, const gte_plan* plan, int dtype, int H, int 
   const size_t es = elem_size(dtype);
   a.vec_qk = dk == dht && (ldq * es) % 16 == 0 && aligned16(q) && aligned16(k) && aligned16(dq) && aligned16(dk_out);
   a.vec_v = dv == dht && (ldv * es) % 16 == 0 && aligned16(v) && aligned16(out) && aligned16(dout) && aligned16(dv_out);
-  const int lph = fast_lph(dtype, H, dk, dv, ldq, ldv, {q, k, v, out, dout, dq, dk_out, dv_out});
+  const int lph = fast_lph(dtype, plan->rows, H, dk, dv, ldq, ldv, {q, k, v, out, dout, dq, dk_out, dv_out});
   if (lph) {
     CUDA_TRY(dispatch_fast(dtype, kBwdRows, a, lph, c->stream));
     CUDA_TRY(dispatch_fast(dtype, kBwdCols, a, lph, c->stream));

@@ -13,14 +13,17 @@ namespace gte_b200 {
 template <typename T, int LPH, int LPN>
 cudaError_t launch_fast_one(int which, const SparseArgs& a, cudaStream_t st) {
   constexpr int kBlock = 256;
-  constexpr int EPL = GTE_FAST_EPL;
-  int64_t grid = (a.S * 32 + kBlock - 1) / kBlock;
+  // a chunk (SLOTS * EPL edges) must fit the 32 column indices a warp loads
+  constexpr int EPL = GTE_FAST_EPL < LPN ? GTE_FAST_EPL : LPN;
+  SparseArgs b = a;
+  b.rows_per_cta = rows_per_cta_for(a.S);
+  int64_t grid = (a.S + b.rows_per_cta - 1) / b.rows_per_cta;
   if (grid > (1LL << 30)) grid = 1LL << 30;
   if (grid < 1) grid = 1;
   switch (which) {
-    case kFwd: fast_fwd_kernel<T, LPH, LPN, EPL><<<(unsigned)grid, kBlock, 0, st>>>(a); break;
-    case kBwdRows: fast_bwd_rows_kernel<T, LPH, LPN, EPL><<<(unsigned)grid, kBlock, 0, st>>>(a); break;
-    default: fast_bwd_cols_kernel<T, LPH, LPN, EPL><<<(unsigned)grid, kBlock, 0, st>>>(a); break;
+    case kFwd: fast_fwd_kernel<T, LPH, LPN, EPL><<<(unsigned)grid, kBlock, 0, st>>>(b); break;
+    case kBwdRows: fast_bwd_rows_kernel<T, LPH, LPN, EPL><<<(unsigned)grid, kBlock, 0, st>>>(b); break;
+    default: fast_bwd_cols_kernel<T, LPH, LPN, EPL><<<(unsigned)grid, kBlock, 0, st>>>(b); break;
   }
   return cudaGetLastError();
 }
