@@ -1,13 +1,16 @@
 // Dispatch for the memory-level-parallel kernels (attn_fast.cuh).
 #pragma once
 
-#include "attn_fast.cuh"
+#include "attn_rowslot.cuh"
 #include "attn_launch.cuh"
 
 namespace gte_b200 {
 
 #ifndef GTE_FAST_EPL
 #define GTE_FAST_EPL 8
+#endif
+#ifndef GTE_SLOT_EPL
+#define GTE_SLOT_EPL 4
 #endif
 
 template <typename T, int LPH, int LPN>
@@ -20,6 +23,19 @@ cudaError_t launch_fast_one(int which, const SparseArgs& a, cudaStream_t st) {
   int64_t grid = (a.S + b.rows_per_cta - 1) / b.rows_per_cta;
   if (grid > (1LL << 30)) grid = 1LL << 30;
   if (grid < 1) grid = 1;
+  static const bool warp_rows = [] {
+    const char* e = getenv("GTE_SCHED");
+    return e && e[0] == 'w';
+  }();
+  if (!warp_rows) {  // default: row-slot schedule (attn_rowslot.cuh)
+    constexpr int EPLS = GTE_SLOT_EPL;
+    switch (which) {
+      case kFwd: slot_fwd_kernel<T, LPH, LPN, EPLS><<<(unsigned)grid, kBlock, 0, st>>>(b); break;
+      case kBwdRows: slot_bwd_rows_kernel<T, LPH, LPN, EPLS><<<(unsigned)grid, kBlock, 0, st>>>(b); break;
+      default: slot_bwd_cols_kernel<T, LPH, LPN, EPLS><<<(unsigned)grid, kBlock, 0, st>>>(b); break;
+    }
+    return cudaGetLastError();
+  }
   switch (which) {
     case kFwd: fast_fwd_kernel<T, LPH, LPN, EPL><<<(unsigned)grid, kBlock, 0, st>>>(b); break;
     case kBwdRows: fast_bwd_rows_kernel<T, LPH, LPN, EPL><<<(unsigned)grid, kBlock, 0, st>>>(b); break;
