@@ -87,7 +87,7 @@ def test_layout_golden_cases(cuda, golden):
             assert np.array_equal(L.pattern.row_offsets, d[sp + "pat_ro"])
 
 
-@pytest.mark.parametrize("n,k,db,mult", [(8192, 8, 16, 5.0), (12000, 4, 8, 1.0), (6000, 8, 4, 10.0)])
+@pytest.mark.parametrize("n,k,db,mult", [(8192, 8, 16, 5.0), (3000, 4, 8, 1.0), (2000, 8, 4, 3.0)])
 def test_community_pipeline_vs_oracle(cuda, orc, n, k, db, mult):
     ro, co = community_graph(n, 12.0, community=128, seed=n)
     g = G(ro, co)
