@@ -151,6 +151,41 @@ int gte_layout_pattern_device(const gte_layout* L, const int32_t** d_row_ptr, co
 int gte_layout_pattern_host(const gte_layout* L, int64_t* row_off, int64_t* cols);
 int gte_layout_destroy(gte_layout* L);
 
+/* Host-pointer twins of the builders (int64 reference CSR in host memory;
+ * H2D, GPU build, D2H; synchronous). Capacities as for the device versions. */
+int gte_graph_from_edges_host(gte_ctx* ctx, int64_t n, int64_t m, const int64_t* src, const int64_t* dst,
+                              int64_t* row_off, int64_t* cols, int64_t* nnz_out);
+int gte_add_self_loops_host(gte_ctx* ctx, int64_t n, int64_t nnz, const int64_t* row_off, const int64_t* cols,
+                            int64_t* out_row_off, int64_t* out_cols, int64_t* nnz_out);
+int gte_permute_graph_host(gte_ctx* ctx, int64_t n, int64_t nnz, const int64_t* row_off, const int64_t* cols,
+                           const int64_t* forward, int64_t* out_row_off, int64_t* out_cols);
+int gte_build_cluster_grid_host(gte_ctx* ctx, int64_t n, int64_t nnz, const int64_t* row_off, const int64_t* cols,
+                                const int64_t* forward, int64_t k, int64_t* bnd, int64_t* cell_nnz,
+                                double* cell_density);
+int gte_build_layout_host(gte_ctx* ctx, int64_t n, int64_t nnz, const int64_t* row_off, const int64_t* cols,
+                          int64_t k, const int64_t* bnd, const int64_t* cell_nnz, const double* cell_density,
+                          int strategy, double beta_thre, double beta_g, int64_t d_b, gte_layout** out);
+
+/* ---- host control logic (reference reformation.cpp:224-296,
+ * interleave.cpp:68-106, parallel.cpp:96-113) ---- */
+typedef struct gte_tuner gte_tuner;
+int gte_tuner_create(double beta_g, int64_t delta, gte_tuner** out);
+int gte_tuner_update(gte_tuner* st, double loss, double epoch_time_s, int64_t epoch);
+int gte_tuner_state(const gte_tuner* st, double* avg_loss, int64_t* idx, double* thresholds, int64_t* n_thresholds,
+                    int32_t* has_loss);
+int gte_tuner_history(const gte_tuner* st, int64_t* epochs, double* ldr, int64_t* n);
+int gte_tuner_set(gte_tuner* st, double avg_loss, int64_t idx, int32_t has_loss, int64_t n_hist,
+                  const int64_t* epochs, const double* ldr);
+int gte_tuner_destroy(gte_tuner* st);
+int gte_select_k(int64_t l2_bytes, int64_t hidden_dim, int64_t i, int64_t* out);
+int gte_select_db(int64_t n, const int64_t* db, const double* thr, int64_t* out);
+/* flags[3] = {c1_self_attend, c2_pass, c3_reachable_within_l};
+ * ints[4] = {layers, sweep_from, sweep_to, diameter_lower_bound} */
+int gte_check_conditions(int64_t n, int64_t nnz, const int64_t* row_off, const int64_t* cols, int64_t layers,
+                         int32_t* flags, int64_t* ints);
+int gte_select_mode(const int32_t* flags, int64_t epoch, int64_t dense_period, int32_t* mode, int32_t* reason);
+int gte_partition_sequence(int64_t seq_len, int64_t num_workers, uint64_t seed, int64_t* ids, int64_t* padded);
+
 #ifdef __cplusplus
 }
 #endif

@@ -639,3 +639,119 @@ int gte_layout_destroy(gte_layout* L) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Host-pointer twins (int64 reference CSR in host memory).
+namespace {
+
+struct HostCsr32 {
+  DBuf<int32_t> rp, cl;
+  int alloc_copy(int64_t n, int64_t nnz, const int64_t* row_off, const int64_t* cols, cudaStream_t st) {
+    std::vector<int32_t> r(n + 1), c(nnz > 0 ? nnz : 1);
+    for (int64_t i = 0; i <= n; ++i) r[i] = (int32_t)row_off[i];
+    for (int64_t i = 0; i < nnz; ++i) c[i] = (int32_t)cols[i];
+    GCUDA(rp.alloc(n + 1, st));
+    GCUDA(cl.alloc(nnz, st));
+    GCUDA(cudaMemcpyAsync(rp.p, r.data(), sizeof(int32_t) * (n + 1), cudaMemcpyHostToDevice, st));
+    if (nnz) GCUDA(cudaMemcpyAsync(cl.p, c.data(), sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, st));
+    GCUDA(cudaStreamSynchronize(st));
+    return GTE_OK;
+  }
+};
+
+int d2h_csr(int64_t n, int64_t nnz, const int32_t* d_rp, const int32_t* d_cl, int64_t* row_off, int64_t* cols,
+            cudaStream_t st) {
+  std::vector<int32_t> r(n + 1), c(nnz > 0 ? nnz : 1);
+  GCUDA(cudaMemcpyAsync(r.data(), d_rp, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost, st));
+  if (nnz) GCUDA(cudaMemcpyAsync(c.data(), d_cl, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost, st));
+  GCUDA(cudaStreamSynchronize(st));
+  for (int64_t i = 0; i <= n; ++i) row_off[i] = r[i];
+  for (int64_t i = 0; i < nnz; ++i) cols[i] = c[i];
+  return GTE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gte_graph_from_edges_host(gte_ctx* c, int64_t n, int64_t m, const int64_t* src, const int64_t* dst,
+                              int64_t* row_off, int64_t* cols, int64_t* nnz_out) {
+  if (n < 0) return set_error(GTE_DATA, "graph_from_edges: negative node count");
+  for (int64_t e = 0; e < m; ++e) {  // graph.cpp:51-54, first offending endpoint in edge order
+    if (src[e] < 0 || src[e] >= n)
+      return set_error(GTE_DATA, "graph_from_edges: node id " + std::to_string(src[e]) + " out of range [0, " +
+                                     std::to_string(n) + ")");
+    if (dst[e] < 0 || dst[e] >= n)
+      return set_error(GTE_DATA, "graph_from_edges: node id " + std::to_string(dst[e]) + " out of range [0, " +
+                                     std::to_string(n) + ")");
+  }
+  if (n >= INT_MAX || m >= INT_MAX) return set_error(GTE_CONFIG, "graph_from_edges: exceeds int32 device index range");
+  cudaStream_t st = (cudaStream_t)ctx_stream(c);
+  std::vector<int32_t> s(m > 0 ? m : 1), d(m > 0 ? m : 1);
+  for (int64_t e = 0; e < m; ++e) {
+    s[e] = (int32_t)src[e];
+    d[e] = (int32_t)dst[e];
+  }
+  DBuf<int32_t> ds, dd, rp, cl;
+  GCUDA(ds.alloc(m, st));
+  GCUDA(dd.alloc(m, st));
+  GCUDA(rp.alloc(n + 1, st));
+  GCUDA(cl.alloc(m, st));
+  GCUDA(cudaMemcpyAsync(ds.p, s.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, st));
+  GCUDA(cudaMemcpyAsync(dd.p, d.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, st));
+  int rc = gte_graph_from_edges(c, n, m, ds.p, dd.p, rp.p, cl.p, nnz_out);
+  if (rc) return rc;
+  return d2h_csr(n, *nnz_out, rp.p, cl.p, row_off, cols, st);
+}
+
+int gte_add_self_loops_host(gte_ctx* c, int64_t n, int64_t nnz, const int64_t* row_off, const int64_t* cols,
+                            int64_t* out_row_off, int64_t* out_cols, int64_t* nnz_out) {
+  cudaStream_t st = (cudaStream_t)ctx_stream(c);
+  HostCsr32 in;
+  int rc = in.alloc_copy(n, nnz, row_off, cols, st);
+  if (rc) return rc;
+  DBuf<int32_t> rp, cl;
+  GCUDA(rp.alloc(n + 1, st));
+  GCUDA(cl.alloc(nnz + n, st));
+  rc = gte_add_self_loops(c, n, nnz, in.rp.p, in.cl.p, rp.p, cl.p, nnz_out);
+  if (rc) return rc;
+  return d2h_csr(n, *nnz_out, rp.p, cl.p, out_row_off, out_cols, st);
+}
+
+int gte_permute_graph_host(gte_ctx* c, int64_t n, int64_t nnz, const int64_t* row_off, const int64_t* cols,
+                           const int64_t* forward, int64_t* out_row_off, int64_t* out_cols) {
+  cudaStream_t st = (cudaStream_t)ctx_stream(c);
+  HostCsr32 in;
+  int rc = in.alloc_copy(n, nnz, row_off, cols, st);
+  if (rc) return rc;
+  DBuf<int32_t> rp, cl;
+  GCUDA(rp.alloc(n + 1, st));
+  GCUDA(cl.alloc(nnz, st));
+  rc = gte_permute_graph(c, n, nnz, in.rp.p, in.cl.p, forward, rp.p, cl.p);
+  if (rc) return rc;
+  return d2h_csr(n, nnz, rp.p, cl.p, out_row_off, out_cols, st);
+}
+
+int gte_build_cluster_grid_host(gte_ctx* c, int64_t n, int64_t nnz, const int64_t* row_off, const int64_t* cols,
+                                const int64_t* forward, int64_t k, int64_t* bnd, int64_t* cell_nnz,
+                                double* cell_density) {
+  if (k < 1 || k > n) return set_error(GTE_CONFIG, "build_cluster_grid: invalid k");
+  cudaStream_t st = (cudaStream_t)ctx_stream(c);
+  HostCsr32 in;
+  int rc = in.alloc_copy(n, nnz, row_off, cols, st);
+  if (rc) return rc;
+  return gte_build_cluster_grid(c, n, nnz, in.rp.p, in.cl.p, forward, k, bnd, cell_nnz, cell_density);
+}
+
+int gte_build_layout_host(gte_ctx* c, int64_t n, int64_t nnz, const int64_t* row_off, const int64_t* cols,
+                          int64_t k, const int64_t* bnd, const int64_t* cell_nnz, const double* cell_density,
+                          int strategy, double beta_thre, double beta_g, int64_t d_b, gte_layout** out) {
+  cudaStream_t st = (cudaStream_t)ctx_stream(c);
+  HostCsr32 in;
+  int rc = in.alloc_copy(n, nnz, row_off, cols, st);
+  if (rc) return rc;
+  return gte_build_layout(c, n, nnz, in.rp.p, in.cl.p, k, bnd, cell_nnz, cell_density, strategy, beta_thre, beta_g,
+                          d_b, out);
+}
+
+}  // extern "C"
