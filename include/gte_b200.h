@@ -33,7 +33,11 @@ typedef enum {
 
 typedef enum { GTE_F64 = 0, GTE_F32 = 1, GTE_BF16 = 2 } gte_dtype;
 
-enum { GTE_FORBID_EMPTY_ROWS = 1 };
+/* flags: GTE_FORBID_EMPTY_ROWS raises DataError on a row with no pairs
+ * (edge_sparse_attention, attention.cpp:119-123); GTE_IGNORE_NONFINITE skips
+ * the Q/K/V finiteness error (the reference's backward recomputes the softmax
+ * without checking, attention.cpp:241-320). */
+enum { GTE_FORBID_EMPTY_ROWS = 1, GTE_IGNORE_NONFINITE = 2 };
 
 typedef struct gte_ctx gte_ctx;
 typedef struct gte_plan gte_plan;

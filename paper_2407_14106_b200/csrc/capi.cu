@@ -137,14 +137,15 @@ int reset_err(gte_ctx* c) {
 
 // Reads the latched device errors (synchronising), maps them to the
 // reference's DataError messages (proj/src/attention.cpp:20-22, 119-123).
-int drain_errors(gte_ctx* c) {
+int drain_errors(gte_ctx* c, bool ignore_nonfinite = false) {
   CUDA_TRY(cudaMemcpyAsync(c->h_err, c->d_err, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
-  const int bits = c->h_err[0], row = c->h_err[1];
-  if (bits == 0 && row == INT_MAX) return GTE_OK;
+  const int bits = ignore_nonfinite ? 0 : c->h_err[0], row = c->h_err[1];
+  if (c->h_err[0] == 0 && row == INT_MAX) return GTE_OK;
   int rc = reset_err(c);
   if (rc) return rc;
   CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (bits == 0 && row == INT_MAX) return GTE_OK;
   if (bits & 1) return fail(GTE_DATA, "attention: non-finite Q");
   if (bits & 2) return fail(GTE_DATA, "attention: non-finite K");
   if (bits & 4) return fail(GTE_DATA, "attention: non-finite V");
@@ -511,7 +512,7 @@ int gte_sparse_attn_fwd_host(gte_ctx* c, const gte_plan* plan, int dtype, int H,
                            (int64_t)H * dv, bias ? c->io[5].p : nullptr, wmult ? c->io[6].p : nullptr,
                            c->io[3].p, c->io[4].p, flags);
   if (rc) return rc;
-  rc = drain_errors(c);
+  rc = drain_errors(c, (flags & GTE_IGNORE_NONFINITE) != 0);
   if (rc) return rc;
   CUDA_TRY(cudaMemcpyAsync(out, c->io[3].p, bv, cudaMemcpyDeviceToHost, st));
   if (lse_out) CUDA_TRY(cudaMemcpyAsync(lse_out, c->io[4].p, S * H * as, cudaMemcpyDeviceToHost, st));
