@@ -47,14 +47,41 @@ def algorithmic_bytes(S, E, e):
     return 12 * e * S * H * DH + 8 * S * H + 8 * (S + 1) + 20 * E
 
 
-def make_workload(seed=7):
+def make_workload(seed=7, pattern="ecr", info=None):
+    """C3 sequence -> attention pattern, as the reference Trainer prepares it
+    (proj/src/model.cpp:378-392, 437-468): node ids shuffled, cluster-aware
+    reorder (k = 8, seed 1), permuted graph, k x k grid, Elastic layout at
+    beta_thre = 5 beta_G with d_b = 16. pattern="edge" skips ECR
+    (topology-induced pattern in reordered coordinates). Preprocessing times
+    go to `info` (excluded from the timed step, as gte_main.cpp:171-175)."""
+    from paper_2407_14106_b200 import partition as P
+    from paper_2407_14106_b200.attention import Graph
     from paper_2407_14106_b200.datagen import community_graph
 
-    # planted community order (the product reorder keeps clusters contiguous;
-    # see DESIGN.md "bench workload")
-    ro, co = community_graph(262144, 61859140 / 2449029, community=256, intra=0.8, sigma=1.0, seed=seed,
-                             shuffle=False)
-    return ro, co
+    info = {} if info is None else info
+    t0 = time.perf_counter()
+    ro, co = community_graph(262144, 61859140 / 2449029, community=256, intra=0.8, sigma=1.0, seed=seed, shuffle=True)
+    g = Graph(262144, ro, co)
+    info["generate_s"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    perm = P.reorder(g, 8, 1)
+    info["reorder_s"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    grid = P.build_cluster_grid(g, perm, 8)
+    gp = P.permute_graph(g, perm)
+    info["grid_permute_s"] = time.perf_counter() - t0
+    info["diag_edge_fraction"] = P.diagonal_edge_fraction(grid)
+    info["graph_E"] = int(g.nnz())
+    if pattern == "edge":
+        return np.asarray(gp.row_offsets), np.asarray(gp.col_indices)
+    bg = P.density(g)
+    t0 = time.perf_counter()
+    L = P.build_layout(grid, gp, P.ELASTIC, 5 * bg, bg, 16)
+    info["layout_s"] = time.perf_counter() - t0
+    info["transferred_cells"] = L.transferred_cells()
+    info["subblocks"] = L.subblock_count()
+    info["dropped_edges"] = int(L.dropped_edges)
+    return np.asarray(L.pattern.row_offsets), np.asarray(L.pattern.cols)
 
 
 class ClockSampler:
@@ -150,18 +177,43 @@ def cpu_baseline(ro, co, sample_rows=131072, steps=3, warmup=1, threads=None):
             "sample": f"rows [0,{rows}), {H} heads sequential, C oracle port"}
 
 
+def cached_workload(pattern, info):
+    """make_workload with a best-effort on-disk cache (same inputs -> same
+    pattern; the cache only saves the ~1 min host reorder on repeat runs)."""
+    path = os.path.join(tempfile.gettempdir(), f"gte_c3_{pattern}_v1.npz")
+    if os.path.exists(path):
+        try:
+            d = np.load(path, allow_pickle=False)
+            info.update(json.loads(str(d["info"])))
+            info["cached"] = True
+            return d["ro"], d["co"]
+        except Exception:
+            pass
+    ro, co = make_workload(pattern=pattern, info=info)
+    try:
+        np.savez(path, ro=ro, co=co, info=np.array(json.dumps(info)))
+    except OSError:
+        pass
+    return ro, co
+
+
 def run_reference_arm(args, rank, world):
     if rank != 0:
         return
-    ro, co = make_workload()
+    import torch
+
+    torch.cuda.set_device(0)  # pattern preparation only; the timed path is the CPU reference
+    info = {}
+    ro, co = cached_workload(args.pattern, info)
     steps = max(1, args.steps)
     res = cpu_baseline(ro, co, sample_rows=32768, steps=steps, warmup=max(0, min(args.warmup, 1)))
     line = {"metric": METRIC, "value": res["value"], "unit": "nodes/s", "n_gpus": args.gpus, "steps": steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(res.get("step_s", [0.0])),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": "C3 products-shaped S=262144 H=8 dh=8 (bounded row sample)", "S": 262144,
-                       "E": int(co.shape[0]), "heads": H, "head_dim": DH},
+            "config": {"workload": "C3 products-shaped S=262144 H=8 dh=8, reorder k=8 + ECR 5*beta_G d_b=16 "
+                                   "(bounded row sample)", "S": 262144, "E": int(co.shape[0]), "heads": H,
+                       "head_dim": DH, "pattern": args.pattern},
             "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": res["value"], "unit": "nodes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -176,6 +228,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (profiling runs)")
+    ap.add_argument("--pattern", default="ecr", choices=["ecr", "edge"],
+                    help="ecr: reorder + Elastic layout (default, the C3 config); edge: reordered graph pattern")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -195,7 +249,8 @@ def main():
     from paper_2407_14106_b200 import attention as A
 
     args.warmup = max(3, args.warmup)
-    ro, co = make_workload()
+    info = {}
+    ro, co = cached_workload(args.pattern, info)
     S, E = ro.shape[0] - 1, co.shape[0]
     dev = torch.device("cuda", local)
     td = torch.float32 if args.dtype == "f32" else torch.bfloat16
@@ -289,9 +344,10 @@ def main():
         "metric": METRIC, "value": world * S / (ms * 1e-3), "unit": "nodes/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": args.dtype, "data": "synthetic",
-        "config": {"workload": "C3 ogbn-products-shaped community graph, S=262144, GPH-slim H=8 dh=8, "
-                               "topology-induced pattern in planted cluster order",
-                   "S": S, "E": int(E), "heads": H, "head_dim": DH, "pattern": "edge+self-loops",
+        "config": {"workload": "C3 ogbn-products-shaped community graph (ids shuffled), S=262144, GPH-slim H=8 "
+                               "dh=8, cluster reorder k=8 + Elastic reformation beta_thre=5*beta_G d_b=16",
+                   "S": S, "E": int(E), "heads": H, "head_dim": DH, "pattern": args.pattern,
+                   "preprocess": info,
                    "parallelism": f"replicas x{world}" if world > 1 else "single",
                    "l2": "flushed between timed steps (2x126MB write); inputs 8x" + f"{S*H*DH*e/2**20:.0f}MB > L2"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,

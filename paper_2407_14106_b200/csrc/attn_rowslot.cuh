@@ -141,8 +141,9 @@ __global__ void __launch_bounds__(256) slot_fwd_kernel(SparseArgs p) {
             if (g.part == 0) LSE[(int64_t)i * p.H + g.hl] = M::neg_inf();
           }
         } else if (g.head_ok) {
+          const float inv = __frcp_rn(l);  // l == 1 (degree-1 rows) stays exact
 #pragma unroll
-          for (int t = 0; t < VW; ++t) acc[t] = __fdiv_rn(acc[t], l);
+          for (int t = 0; t < VW; ++t) acc[t] *= inv;
           *reinterpret_cast<uint4*>(O + (uint32_t)i * rv + g.bo) = P::pack(acc);
           if (g.part == 0) LSE[(int64_t)i * p.H + g.hl] = m + M::lg(l);
         }

@@ -27,12 +27,23 @@ cudaError_t launch_fast_one(int which, const SparseArgs& a, cudaStream_t st) {
     const char* e = getenv("GTE_SCHED");
     return e && e[0] == 'w';
   }();
+  static const int slot_epl = [] {
+    const char* e = getenv("GTE_SLOT_EPL");
+    return e ? atoi(e) : GTE_SLOT_EPL;
+  }();
   if (!warp_rows) {  // default: row-slot schedule (attn_rowslot.cuh)
-    constexpr int EPLS = GTE_SLOT_EPL;
+    if (slot_epl >= 8) {
+      switch (which) {
+        case kFwd: slot_fwd_kernel<T, LPH, LPN, 8><<<(unsigned)grid, kBlock, 0, st>>>(b); break;
+        case kBwdRows: slot_bwd_rows_kernel<T, LPH, LPN, 8><<<(unsigned)grid, kBlock, 0, st>>>(b); break;
+        default: slot_bwd_cols_kernel<T, LPH, LPN, 8><<<(unsigned)grid, kBlock, 0, st>>>(b); break;
+      }
+      return cudaGetLastError();
+    }
     switch (which) {
-      case kFwd: slot_fwd_kernel<T, LPH, LPN, EPLS><<<(unsigned)grid, kBlock, 0, st>>>(b); break;
-      case kBwdRows: slot_bwd_rows_kernel<T, LPH, LPN, EPLS><<<(unsigned)grid, kBlock, 0, st>>>(b); break;
-      default: slot_bwd_cols_kernel<T, LPH, LPN, EPLS><<<(unsigned)grid, kBlock, 0, st>>>(b); break;
+      case kFwd: slot_fwd_kernel<T, LPH, LPN, 4><<<(unsigned)grid, kBlock, 0, st>>>(b); break;
+      case kBwdRows: slot_bwd_rows_kernel<T, LPH, LPN, 4><<<(unsigned)grid, kBlock, 0, st>>>(b); break;
+      default: slot_bwd_cols_kernel<T, LPH, LPN, 4><<<(unsigned)grid, kBlock, 0, st>>>(b); break;
     }
     return cudaGetLastError();
   }
