@@ -13,6 +13,7 @@
 
 #include "../../include/gte_b200.h"
 #include "fast_launch.cuh"
+#include "prefetch.cuh"
 
 using namespace gte_b200;
 
@@ -255,6 +256,36 @@ int fast_lph(int dtype, int64_t S, int H, int dk, int dv, int64_t ldq, int64_t l
   return lph;
 }
 
+bool prefetch_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("GTE_L2_PREFETCH");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+}  // namespace
+// (gte_ctx is defined below; forward helper)
+static cudaError_t l2_prefetch_impl(cudaStream_t st, int64_t* launches, std::initializer_list<const void*> ptrs,
+                                    std::initializer_list<size_t> bytes) {
+  PrefetchArgs pa{};
+  int n = 0;
+  auto b = bytes.begin();
+  for (const void* p : ptrs) {
+    pa.ptr[n] = static_cast<const char*>(p);
+    pa.bytes[n] = *b++;
+    ++n;
+  }
+  pa.n = n;
+  l2_prefetch_kernel<<<148, 32, 0, st>>>(pa);
+  *launches += 1;
+  return cudaGetLastError();
+}
+static cudaError_t l2_prefetch(gte_ctx* c, std::initializer_list<const void*> ptrs, std::initializer_list<size_t> bytes) {
+  return l2_prefetch_impl(c->stream, &c->launches, ptrs, bytes);
+}
+namespace {
+
 cudaError_t dispatch_fast(int dtype, int which, const SparseArgs& a, int lph, cudaStream_t st) {
   int lpn = 1;
   while (lpn < a.H) lpn <<= 1;
@@ -435,6 +466,10 @@ int gte_sparse_attn_fwd(gte_ctx* c, const gte_plan* plan, int dtype, int H, int 
   a.vec_v = dv == dht && (ldv * es) % 16 == 0 && aligned16(v) && aligned16(out);
   if (plan->rows == 0) return GTE_OK;
   const int lph = fast_lph(dtype, plan->rows, H, dk, dv, ldq, ldv, {q, k, v, out});
+  if (lph && prefetch_enabled()) {
+    const size_t rows = (size_t)plan->rows;
+    CUDA_TRY(l2_prefetch(c, {k, v}, {rows * ldq * es, rows * ldv * es}));
+  }
   if (lph)
     CUDA_TRY(dispatch_fast(dtype, kFwd, a, lph, c->stream));
   else
@@ -478,7 +513,14 @@ int gte_sparse_attn_bwd(gte_ctx* c, const gte_plan* plan, int dtype, int H, int 
   a.vec_v = dv == dht && (ldv * es) % 16 == 0 && aligned16(v) && aligned16(out) && aligned16(dout) && aligned16(dv_out);
   const int lph = fast_lph(dtype, plan->rows, H, dk, dv, ldq, ldv, {q, k, v, out, dout, dq, dk_out, dv_out});
   if (lph) {
+    const size_t rows = (size_t)plan->rows;
+    if (prefetch_enabled()) {
+      CUDA_TRY(l2_prefetch(c, {k, v}, {rows * ldq * es, rows * ldv * es}));
+    }
     CUDA_TRY(dispatch_fast(dtype, kBwdRows, a, lph, c->stream));
+    if (prefetch_enabled()) {
+      CUDA_TRY(l2_prefetch(c, {q, dout}, {rows * ldq * es, rows * ldv * es}));
+    }
     CUDA_TRY(dispatch_fast(dtype, kBwdCols, a, lph, c->stream));
   } else {
     CUDA_TRY(dispatch(dtype, kBwdRows, a, dht, lpn, c->stream));
