@@ -69,6 +69,20 @@ int gte_plan_shape(const gte_plan* plan, int64_t* rows, int64_t* nnz, int64_t* m
 /* device pointers of the plan's int32 CSR/CSC (for fused callers) */
 int gte_plan_device_csr(const gte_plan* plan, const int32_t** row_ptr, const int32_t** cols);
 
+/* ---- execution schedule (no reference counterpart: an execution order only;
+ * results are bit-identical with or without it) ----
+ * gte_community_order: host, synchronous label propagation over the
+ *   symmetrised pattern (`iters` rounds max), rows ordered by (label, row);
+ *   order[n] receives the row sequence (csrc/schedule.cpp).
+ * gte_plan_schedule: the same on a plan's CSR, stored on the device; the
+ *   sparse kernels then execute rows (and CSC columns) in that order so a
+ *   CTA's gathers hit rows its neighbours just pulled into L1.
+ * gte_plan_set_order: any permutation of [0, rows) (NULL clears). */
+int gte_community_order(int64_t n, int64_t nnz, const int64_t* row_off, const int64_t* cols, int64_t iters,
+                        int64_t* order, int64_t* n_communities);
+int gte_plan_schedule(gte_plan* plan, int64_t iters, int64_t* n_communities);
+int gte_plan_set_order(gte_plan* plan, const int64_t* order);
+
 /* ---- sparse (topology-induced) attention over a plan, all heads at once ----
  * Replaces sparse_attention / sparse_attention_backward (reference
  * proj/src/attention.cpp:96-162, 241-320) called per head, and the per-head

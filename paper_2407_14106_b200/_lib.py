@@ -78,6 +78,9 @@ def lib() -> C.CDLL:
             L.gte_plan_destroy.argtypes = [VP]
             L.gte_plan_shape.argtypes = [VP, C.POINTER(I64), C.POINTER(I64), C.POINTER(I64), C.POINTER(I64)]
             L.gte_plan_device_csr.argtypes = [VP, C.POINTER(VP), C.POINTER(VP)]
+            L.gte_community_order.argtypes = [I64, I64, VP, VP, I64, VP, C.POINTER(I64)]
+            L.gte_plan_schedule.argtypes = [VP, I64, C.POINTER(I64)]
+            L.gte_plan_set_order.argtypes = [VP, VP]
             L.gte_sparse_attn_fwd.argtypes = [VP, VP, I32, I32, I32, I32, VP, VP, I64, VP, I64, VP, VP, VP, VP, I32]
             L.gte_sparse_attn_bwd.argtypes = [VP, VP, I32, I32, I32, I32, VP, VP, I64, VP, I64, VP, VP, VP, VP, VP,
                                               VP, VP, VP, VP]

@@ -124,6 +124,20 @@ class Context:
         return int(_lib.lib().gte_ctx_launches(self.h))
 
 
+def community_order(row_offsets, cols, iters: int = 20):
+    """Host label-propagation execution order of a CSR pattern
+    (gte_community_order); returns (order int64[n], communities)."""
+    ro = np.ascontiguousarray(row_offsets, dtype=np.int64)
+    co = np.ascontiguousarray(cols, dtype=np.int64)
+    n = ro.shape[0] - 1
+    out = np.empty(max(n, 1), dtype=np.int64)
+    nc = C.c_int64()
+    cp = co if co.shape[0] else np.zeros(1, dtype=np.int64)
+    check(_lib.lib().gte_community_order(n, co.shape[0], ro.ctypes.data, cp.ctypes.data, iters, out.ctypes.data,
+                                         C.byref(nc)))
+    return out[:n], nc.value
+
+
 class DevicePlan:
     """gte_plan: the pattern resident in HBM as int32 CSR + CSC."""
 
@@ -160,6 +174,23 @@ class DevicePlan:
         check(_lib.lib().gte_plan_create_device(ctx.h, rows, nnz, C.c_void_p(row_ptr_ptr), C.c_void_p(cols_ptr),
                                                 C.byref(h)))
         return cls(h, ctx)
+
+    def schedule(self, iters: int = 20) -> int:
+        """Community execution order (label propagation, csrc/schedule.cpp);
+        returns the number of communities. Results are unchanged."""
+        n = C.c_int64()
+        check(_lib.lib().gte_plan_schedule(self.h, iters, C.byref(n)))
+        return n.value
+
+    def set_order(self, order) -> None:
+        """Explicit execution order (a permutation of the rows); None clears."""
+        if order is None:
+            check(_lib.lib().gte_plan_set_order(self.h, None))
+            return
+        o = np.ascontiguousarray(order, dtype=np.int64)
+        if o.shape[0] != self.rows:
+            raise ConfigError("plan: order length must equal the row count")
+        check(_lib.lib().gte_plan_set_order(self.h, o.ctypes.data))
 
     def close(self):
         if self.h:

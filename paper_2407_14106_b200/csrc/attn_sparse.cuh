@@ -60,6 +60,18 @@ struct SparseArgs {
   // warps stride through it. Contiguous ranges keep a cluster-ordered
   // sequence's neighbour rows hot in that SM's L1.
   int64_t rows_per_cta = 8;
+  // tile kernels (attn_tile.cuh): execution plan of the CSR pass (order of
+  // the non-hub rows, tile boundaries into it, hub rows) and of the CSC pass
+  // (same over columns), and the packed (lse, delta) workspace [S x H] float2
+  // written by the CSR pass for the CSC pass.
+  const int32_t* order = nullptr;
+  const int32_t* tiles = nullptr;
+  const int32_t* hubs = nullptr;
+  const int32_t* order_c = nullptr;
+  const int32_t* tiles_c = nullptr;
+  const int32_t* hubs_c = nullptr;
+  int n_tiles = 0, n_hubs = 0, n_tiles_c = 0, n_hubs_c = 0;
+  void* lsedelta = nullptr;
 };
 
 struct WarpRange {

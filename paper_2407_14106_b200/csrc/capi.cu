@@ -1,6 +1,7 @@
 // C ABI of the B200 graph-attention library (include/gte_b200.h): context,
 // device pattern plans (CSR + CSC built on the GPU with radix sort/scan), and
 // the sparse attention entries with their host-pointer twins.
+#include <algorithm>
 #include <climits>
 #include <cstdlib>
 #include <initializer_list>
@@ -13,6 +14,7 @@
 
 #include "../../include/gte_b200.h"
 #include "fast_launch.cuh"
+#include "tile_launch.cuh"
 #include "prefetch.cuh"
 
 using namespace gte_b200;
@@ -114,7 +116,7 @@ struct gte_ctx {
   int* d_err = nullptr;  // [0] non-finite bits, [1] first empty row
   int* h_err = nullptr;  // pinned mirror
   int64_t launches = 0;
-  DevBuf io[12];
+  DevBuf io[13];  // [11] delta (generic), [12] packed (lse, delta) (tile)
 };
 
 struct gte_plan {
@@ -126,6 +128,14 @@ struct gte_plan {
   int32_t* csc_row = nullptr;
   int32_t* csc_eid = nullptr;
   int32_t* unref = nullptr;
+  // execution plan of the tile kernels (build_exec): per pass the order of the
+  // non-hub rows (columns), tile boundaries into it, and the hub list
+  int32_t* exec = nullptr;  // one allocation holding the six arrays below
+  const int32_t *order = nullptr, *tiles = nullptr, *hubs = nullptr;
+  const int32_t *order_c = nullptr, *tiles_c = nullptr, *hubs_c = nullptr;
+  int n_tiles = 0, n_hubs = 0, n_tiles_c = 0, n_hubs_c = 0;
+  bool scheduled = false;
+  int64_t communities = 0;
 };
 
 namespace {
@@ -213,6 +223,77 @@ int build_plan_device(gte_ctx* c, gte_plan* p) {
   return GTE_OK;
 }
 
+// Execution plan of the tile kernels (attn_tile.cuh) for both passes: walk
+// the execution order (given, or natural), send rows (columns) longer than
+// kHubDegree to the hub list, cut the rest into tiles of <= kTileRows rows
+// and <= kTileCap edges, and order each tile longest-first (its slots then
+// finish together). An execution order only: outputs do not depend on it.
+int build_exec(gte_plan* p, const int64_t* order) {
+  const int64_t n = p->rows;
+  cudaStream_t st = p->ctx->stream;
+  std::vector<int32_t> rp(n + 1), cp(n + 1);
+  CUDA_TRY(cudaMemcpyAsync(rp.data(), p->row_ptr, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(cp.data(), p->col_ptr, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  struct Pass {
+    std::vector<int32_t> order, tiles, hubs;
+  } ps[2];
+  for (int pass = 0; pass < 2; ++pass) {
+    const std::vector<int32_t>& ptr = pass == 0 ? rp : cp;
+    Pass& P = ps[pass];
+    auto deg = [&](int32_t r) { return ptr[r + 1] - ptr[r]; };
+    P.tiles.push_back(0);
+    int rows_in = 0, edges_in = 0;
+    for (int64_t x = 0; x < n; ++x) {
+      const int32_t r = (int32_t)(order ? order[x] : x);
+      const int dg = deg(r);
+      if (dg > kHubDegree) {
+        P.hubs.push_back(r);
+        continue;
+      }
+      if (rows_in == kTileRows || edges_in + dg > kTileCap) {
+        P.tiles.push_back((int32_t)P.order.size());
+        rows_in = edges_in = 0;
+      }
+      P.order.push_back(r);
+      ++rows_in;
+      edges_in += dg;
+    }
+    if (rows_in > 0) P.tiles.push_back((int32_t)P.order.size());
+    for (size_t t = 0; t + 1 < P.tiles.size(); ++t)
+      std::stable_sort(P.order.begin() + P.tiles[t], P.order.begin() + P.tiles[t + 1],
+                       [&](int32_t a, int32_t b) { return deg(a) > deg(b); });
+  }
+  size_t total = 0;
+  for (auto& P : ps) total += P.order.size() + P.tiles.size() + P.hubs.size();
+  cudaFree(p->exec);
+  p->exec = nullptr;
+  CUDA_TRY(cudaMalloc(&p->exec, sizeof(int32_t) * (total + 1)));
+  int32_t* cur = p->exec;
+  const int32_t* where[2][3];
+  for (int pass = 0; pass < 2; ++pass) {
+    std::vector<int32_t>* v[3] = {&ps[pass].order, &ps[pass].tiles, &ps[pass].hubs};
+    for (int a = 0; a < 3; ++a) {
+      where[pass][a] = cur;
+      if (!v[a]->empty())
+        CUDA_TRY(cudaMemcpyAsync(cur, v[a]->data(), sizeof(int32_t) * v[a]->size(), cudaMemcpyHostToDevice, st));
+      cur += v[a]->size();
+    }
+  }
+  CUDA_TRY(cudaStreamSynchronize(st));
+  p->order = where[0][0];
+  p->tiles = where[0][1];
+  p->hubs = where[0][2];
+  p->order_c = where[1][0];
+  p->tiles_c = where[1][1];
+  p->hubs_c = where[1][2];
+  p->n_tiles = (int)ps[0].tiles.size() - 1;
+  p->n_hubs = (int)ps[0].hubs.size();
+  p->n_tiles_c = (int)ps[1].tiles.size() - 1;
+  p->n_hubs_c = (int)ps[1].hubs.size();
+  return GTE_OK;
+}
+
 void free_plan(gte_plan* p) {
   if (!p) return;
   cudaFree(p->row_ptr);
@@ -221,6 +302,7 @@ void free_plan(gte_plan* p) {
   cudaFree(p->csc_row);
   cudaFree(p->csc_eid);
   cudaFree(p->unref);
+  cudaFree(p->exec);
   delete p;
 }
 
@@ -286,10 +368,28 @@ static cudaError_t l2_prefetch(gte_ctx* c, std::initializer_list<const void*> pt
 }
 namespace {
 
-cudaError_t dispatch_fast(int dtype, int which, const SparseArgs& a, int lph, cudaStream_t st) {
+// Kernel schedule for the fast family: 't' tile (default, attn_tile.cuh),
+// 's' row-slot, 'w' warp-per-row (attn_rowslot.cuh / attn_fast.cuh); GTE_SCHED.
+char fast_schedule() {
+  static const char v = [] {
+    const char* e = getenv("GTE_SCHED");
+    return (e && (e[0] == 's' || e[0] == 'w')) ? e[0] : 't';
+  }();
+  return v;
+}
+
+cudaError_t dispatch_fast(int dtype, int which, const SparseArgs& a, int lph, cudaStream_t st, int64_t* launches) {
   int lpn = 1;
   while (lpn < a.H) lpn <<= 1;
   lpn *= lph;
+  if (fast_schedule() == 't') {
+    int n = 0;
+    cudaError_t e = dtype == GTE_F32 ? launch_tile_f32(which, a, lph, lpn, st, &n)
+                                     : launch_tile_bf16(which, a, lph, lpn, st, &n);
+    *launches += n;
+    return e;
+  }
+  *launches += 1;
   return dtype == GTE_F32 ? launch_fast_f32(which, a, lph, lpn, st) : launch_fast_bf16(which, a, lph, lpn, st);
 }
 
@@ -327,6 +427,16 @@ void fill_common(SparseArgs& a, const gte_plan* plan, int dtype, int H, int dk, 
   a.csc_eid = plan->csc_eid;
   a.scale = 1.0 / std::sqrt((double)dk);
   a.err = plan->ctx->d_err;
+  a.order = plan->order;
+  a.tiles = plan->tiles;
+  a.hubs = plan->hubs;
+  a.order_c = plan->order_c;
+  a.tiles_c = plan->tiles_c;
+  a.hubs_c = plan->hubs_c;
+  a.n_tiles = plan->n_tiles;
+  a.n_hubs = plan->n_hubs;
+  a.n_tiles_c = plan->n_tiles_c;
+  a.n_hubs_c = plan->n_hubs_c;
   (void)dtype;
 }
 
@@ -388,6 +498,7 @@ int gte_plan_create_device(gte_ctx* c, int64_t rows, int64_t nnz, const int32_t*
   cudaMemcpyAsync(p->row_ptr, d_row_ptr, sizeof(int32_t) * (rows + 1), cudaMemcpyDeviceToDevice, st);
   if (nnz) cudaMemcpyAsync(p->cols, d_cols, sizeof(int32_t) * nnz, cudaMemcpyDeviceToDevice, st);
   int rc = build_plan_device(c, p);
+  if (rc == GTE_OK) rc = build_exec(p, nullptr);
   if (rc) {
     free_plan(p);
     return rc;
@@ -417,6 +528,7 @@ int gte_plan_create_host(gte_ctx* c, int64_t rows, int64_t nnz, const int64_t* r
   cudaMemcpyAsync(p->row_ptr, ro.data(), sizeof(int32_t) * (rows + 1), cudaMemcpyHostToDevice, st);
   if (nnz) cudaMemcpyAsync(p->cols, co.data(), sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, st);
   int rc = build_plan_device(c, p);  // synchronises before `ro`/`co` go out of scope
+  if (rc == GTE_OK) rc = build_exec(p, nullptr);
   if (rc) {
     free_plan(p);
     return rc;
@@ -445,6 +557,43 @@ int gte_plan_device_csr(const gte_plan* p, const int32_t** rp, const int32_t** c
   return GTE_OK;
 }
 
+int gte_plan_set_order(gte_plan* p, const int64_t* order) {
+  if (!p) return fail(GTE_CONFIG, "plan: null plan");
+  const int64_t n = p->rows;
+  if (order) {
+    std::vector<char> seen(n > 0 ? n : 1, 0);
+    for (int64_t i = 0; i < n; ++i) {
+      const int64_t r = order[i];
+      if (r < 0 || r >= n || seen[r]) return fail(GTE_CONFIG, "plan: order is not a permutation of the rows");
+      seen[r] = 1;
+    }
+  }
+  int rc = build_exec(p, order);
+  if (rc) return rc;
+  p->scheduled = order != nullptr;
+  if (!order) p->communities = 0;
+  return GTE_OK;
+}
+
+int gte_plan_schedule(gte_plan* p, int64_t iters, int64_t* communities) {
+  if (!p) return fail(GTE_CONFIG, "plan: null plan");
+  const int64_t n = p->rows, m = p->nnz;
+  cudaStream_t st = p->ctx->stream;
+  std::vector<int32_t> ro(n + 1), co(m > 0 ? m : 1);
+  CUDA_TRY(cudaMemcpyAsync(ro.data(), p->row_ptr, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost, st));
+  if (m) CUDA_TRY(cudaMemcpyAsync(co.data(), p->cols, sizeof(int32_t) * m, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  std::vector<int64_t> ro64(ro.begin(), ro.end()), co64(co.begin(), co.begin() + m), order(n > 0 ? n : 1);
+  int64_t comms = 0;
+  int rc = gte_community_order(n, m, ro64.data(), co64.data(), iters, order.data(), &comms);
+  if (rc) return rc;
+  rc = gte_plan_set_order(p, order.data());
+  if (rc) return rc;
+  p->communities = comms;
+  if (communities) *communities = comms;
+  return GTE_OK;
+}
+
 int gte_sparse_attn_fwd(gte_ctx* c, const gte_plan* plan, int dtype, int H, int dk, int dv,
                         const void* q, const void* k, int64_t ldq, const void* v, int64_t ldv,
                         const void* bias, const void* wmult, void* out, void* lse, int flags) {
@@ -466,15 +615,16 @@ int gte_sparse_attn_fwd(gte_ctx* c, const gte_plan* plan, int dtype, int H, int 
   a.vec_v = dv == dht && (ldv * es) % 16 == 0 && aligned16(v) && aligned16(out);
   if (plan->rows == 0) return GTE_OK;
   const int lph = fast_lph(dtype, plan->rows, H, dk, dv, ldq, ldv, {q, k, v, out});
-  if (lph && prefetch_enabled()) {
+  if (lph && prefetch_enabled() && fast_schedule() != 't') {
     const size_t rows = (size_t)plan->rows;
     CUDA_TRY(l2_prefetch(c, {k, v}, {rows * ldq * es, rows * ldv * es}));
   }
-  if (lph)
-    CUDA_TRY(dispatch_fast(dtype, kFwd, a, lph, c->stream));
-  else
+  if (lph) {
+    CUDA_TRY(dispatch_fast(dtype, kFwd, a, lph, c->stream, &c->launches));
+  } else {
     CUDA_TRY(dispatch(dtype, kFwd, a, dht, lpn, c->stream));
-  c->launches += 1;
+    c->launches += 1;
+  }
   if (!lph && plan->n_unref > 0) {  // the fast kernels check every row's own K/V
     CUDA_TRY(launch_finite_rows(dtype, k, v, plan->unref, (int)plan->n_unref, ldq, ldv, (int64_t)H * dk,
                                 (int64_t)H * dv, c->d_err, c->stream));
@@ -492,6 +642,8 @@ int gte_sparse_attn_bwd(gte_ctx* c, const gte_plan* plan, int dtype, int H, int 
   if (plan->rows == 0) return GTE_OK;
   DevBuf& ws = c->io[11];
   CUDA_TRY(ws.ensure(acc_size(dtype) * (size_t)plan->rows * H));
+  DevBuf& ws2 = c->io[12];
+  CUDA_TRY(ws2.ensure(2 * sizeof(float) * (size_t)plan->rows * H));
   SparseArgs a;
   fill_common(a, plan, dtype, H, dk, dv, ldq, ldv);
   a.q = q;
@@ -503,6 +655,7 @@ int gte_sparse_attn_bwd(gte_ctx* c, const gte_plan* plan, int dtype, int H, int 
   a.wmult = wmult;
   a.lse = const_cast<void*>(lse);
   a.delta = ws.p;
+  a.lsedelta = ws2.p;
   a.dq = dq;
   a.dk_out = dk_out;
   a.dv_out = dv_out;
@@ -514,19 +667,20 @@ int gte_sparse_attn_bwd(gte_ctx* c, const gte_plan* plan, int dtype, int H, int 
   const int lph = fast_lph(dtype, plan->rows, H, dk, dv, ldq, ldv, {q, k, v, out, dout, dq, dk_out, dv_out});
   if (lph) {
     const size_t rows = (size_t)plan->rows;
-    if (prefetch_enabled()) {
+    const bool pf = prefetch_enabled() && fast_schedule() != 't';
+    if (pf) {
       CUDA_TRY(l2_prefetch(c, {k, v}, {rows * ldq * es, rows * ldv * es}));
     }
-    CUDA_TRY(dispatch_fast(dtype, kBwdRows, a, lph, c->stream));
-    if (prefetch_enabled()) {
+    CUDA_TRY(dispatch_fast(dtype, kBwdRows, a, lph, c->stream, &c->launches));
+    if (pf) {
       CUDA_TRY(l2_prefetch(c, {q, dout}, {rows * ldq * es, rows * ldv * es}));
     }
-    CUDA_TRY(dispatch_fast(dtype, kBwdCols, a, lph, c->stream));
+    CUDA_TRY(dispatch_fast(dtype, kBwdCols, a, lph, c->stream, &c->launches));
   } else {
     CUDA_TRY(dispatch(dtype, kBwdRows, a, dht, lpn, c->stream));
     CUDA_TRY(dispatch(dtype, kBwdCols, a, dht, lpn, c->stream));
+    c->launches += 2;
   }
-  c->launches += 2;
   return GTE_OK;
 }
 

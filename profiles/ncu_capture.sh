@@ -12,7 +12,7 @@ mkdir -p $O
 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file $O/launches_${DT}_${TAG}.csv \
     python bench.py --steps 2 --warmup 3 --dtype $DT --no-cpu-baseline --no-e2e > /dev/null
-ncu --set full --clock-control none --import-source on -k regex:"sparse_|fast_|slot_" -s 9 -c 3 \
+ncu --set full --clock-control none --import-source on -k regex:"sparse_|fast_|slot_|tile_" -s 9 -c 3 \
     -o /tmp/prof_${DT}_${TAG} -f \
     python bench.py --steps 1 --warmup 3 --dtype $DT --no-cpu-baseline --no-e2e > /dev/null
 ncu -i /tmp/prof_${DT}_${TAG}.ncu-rep --page raw --csv > $O/ncu_raw_${DT}_${TAG}.csv

@@ -60,3 +60,24 @@ def test_missing_library_fails_loudly(monkeypatch, tmp_path):
     monkeypatch.setattr(_lib, "_lib", None)
     with pytest.raises(ImportError, match="not built"):
         _lib.lib()
+
+
+def test_community_order_host():
+    """Execution schedule (csrc/schedule.cpp): label propagation recovers the
+    planted communities, the order is a permutation, deterministic."""
+    import numpy as np
+
+    from paper_2407_14106_b200 import attention as A
+    from paper_2407_14106_b200.datagen import community_graph
+
+    ro, co = community_graph(8192, 16.0, community=256, intra=0.9, seed=5, shuffle=True)
+    order, nc = A.community_order(ro, co)
+    assert np.array_equal(np.sort(order), np.arange(8192))
+    assert 16 <= nc <= 64
+    order2, nc2 = A.community_order(ro, co)
+    assert nc2 == nc and np.array_equal(order, order2)
+    # rows of one community are contiguous in the order: most arcs stay inside a 256-row window
+    pos = np.empty(8192, np.int64)
+    pos[order] = np.arange(8192)
+    src = np.repeat(np.arange(8192), np.diff(ro))
+    assert np.mean(np.abs(pos[src] - pos[co]) < 512) > 0.8

@@ -69,7 +69,7 @@ def _torch_dtype(dtype):
     return {"f64": torch.float64, "f32": torch.float32, "bf16": torch.bfloat16}[dtype]
 
 
-def run_device(row_off, cols, H, dh, dtype, seed=0, with_bias=True, with_wm=False, S=None):
+def run_device(row_off, cols, H, dh, dtype, seed=0, with_bias=True, with_wm=False, S=None, order=None):
     """Runs fwd+bwd through DeviceSparseAttention; returns the dtype-rounded fp64
     inputs and the outputs, as numpy fp64."""
     import torch
@@ -84,6 +84,10 @@ def run_device(row_off, cols, H, dh, dtype, seed=0, with_bias=True, with_wm=Fals
     bias = torch.tensor(rng.normal(0, 0.3, E), dtype=acc, device=dev) if with_bias else None
     wm = torch.tensor((rng.random((H, E)) < 0.7) / 0.7, dtype=acc, device=dev) if with_wm else None
     plan = A.DevicePlan.from_host(row_off, cols)
+    if isinstance(order, str) and order == "schedule":
+        plan.schedule()
+    elif order is not None:
+        plan.set_order(order)
     att = A.DeviceSparseAttention(plan, H, dh, dh, dtype)
     out, lse = att.forward(q, k, v, bias, wm)
     dq, dk, dv, db = att.backward(q, k, v, out, lse, do, bias, wm)
@@ -156,6 +160,35 @@ def test_hub_rows_and_columns_f32(cuda, orc):
     want = oracle_multihead(orc, g, r, 8, 8)
     for got, w, nm in zip((r["out"], r["dq"], r["dk"], r["dv"], r["db"]), want, ("out", "dq", "dk", "dv", "dbias")):
         assert_close(got, w, "f32", f"hub {nm}")
+
+
+@pytest.mark.parametrize("dtype,wm", [("f32", False), ("bf16", False), ("f32", True)])
+def test_hub_rows_bf16_and_schedule(cuda, orc, dtype, wm):
+    # hub row/column longer than a tile's staging capacity (global-memory ids)
+    n = 3000
+    s, t = c1_edges(n - 1, 5, 11)
+    glob = n - 1
+    src = np.r_[s, np.arange(n - 1), np.full(n - 1, glob)]
+    dst = np.r_[t, np.full(n - 1, glob), np.arange(n - 1)]
+    ro, co = csr_from_pairs(n, src, dst)
+    g = CSR(n, ro, co)
+    r = run_device(ro, co, 8, 8, dtype, seed=6, order="schedule", with_wm=wm)
+    want = oracle_multihead(orc, g, r, 8, 8)
+    for got, w, nm in zip((r["out"], r["dq"], r["dk"], r["dv"], r["db"]), want, ("out", "dq", "dk", "dv", "dbias")):
+        assert_close(got, w, dtype, f"hub+schedule {nm}")
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_execution_order_is_bit_identical(cuda, dtype):
+    # the community schedule / any execution order changes nothing (each row
+    # is computed by one slot with the same arithmetic, written in place)
+    ro, co = community_graph(20000, 12.0, community=128, seed=3, shuffle=True)
+    base = run_device(ro, co, 8, 8, dtype, seed=4, with_wm=(dtype == "f32"))
+    rnd = np.random.default_rng(0).permutation(20000)
+    for order in ("schedule", rnd):
+        r = run_device(ro, co, 8, 8, dtype, seed=4, with_wm=(dtype == "f32"), order=order)
+        for nm in ("out", "lse", "dq", "dk", "dv", "db"):
+            assert np.array_equal(r[nm], base[nm]), f"{nm} differs under execution order"
 
 
 # ---------------------------------------------------------------- edge semantics
