@@ -11,7 +11,7 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libgte_b200.so")
+LIB_PATH = os.environ.get("GTE_LIB_PATH") or os.path.join(HERE, "libgte_b200.so")  # override: A/B builds
 
 GTE_OK, GTE_CONFIG, GTE_DATA, GTE_DIVERGENCE, GTE_CUDA, GTE_NCCL = 0, 2, 3, 4, 5, 6
 GTE_F64, GTE_F32, GTE_BF16 = 0, 1, 2

@@ -38,8 +38,14 @@ namespace gte_b200 {
 
 constexpr int kTileThreads = 256;
 constexpr int kTileWarps = kTileThreads / 32;
-constexpr int kTileRows = 128;    // rows (columns) per tile, <= kTileThreads
-constexpr int kTileCap = 4096;    // staged edges per tile (32 KB of ids + biases)
+#ifndef GTE_TILE_ROWS
+#define GTE_TILE_ROWS 128
+#endif
+#ifndef GTE_TILE_CAP
+#define GTE_TILE_CAP 4096
+#endif
+constexpr int kTileRows = GTE_TILE_ROWS;  // rows (columns) per tile, <= kTileThreads
+constexpr int kTileCap = GTE_TILE_CAP;    // staged edges per tile (32 KB of ids + biases at 4096)
 constexpr int kTilePad = 8;       // padding slots after the staged edges (>= EPL)
 constexpr int kHubDegree = 1024;  // longer rows/columns go to the hub kernels
 

@@ -15,6 +15,7 @@
 #include "../../include/gte_b200.h"
 #include "fast_launch.cuh"
 #include "tile_launch.cuh"
+#include "wide_launch.cuh"
 #include "prefetch.cuh"
 
 using namespace gte_b200;
@@ -251,13 +252,14 @@ int build_exec(gte_plan* p, const int64_t* order) {
         P.hubs.push_back(r);
         continue;
       }
-      if (rows_in == kTileRows || edges_in + dg > kTileCap) {
+      const int pdg = (dg + 3) / 4 * 4;  // the wide kernels pad rows to 4 edges
+      if (rows_in == kTileRows || edges_in + pdg > kTileCap) {
         P.tiles.push_back((int32_t)P.order.size());
         rows_in = edges_in = 0;
       }
       P.order.push_back(r);
       ++rows_in;
-      edges_in += dg;
+      edges_in += pdg;
     }
     if (rows_in > 0) P.tiles.push_back((int32_t)P.order.size());
     for (size_t t = 0; t + 1 < P.tiles.size(); ++t)
@@ -373,15 +375,56 @@ namespace {
 char fast_schedule() {
   static const char v = [] {
     const char* e = getenv("GTE_SCHED");
-    return (e && (e[0] == 's' || e[0] == 'w')) ? e[0] : 't';
+    return (e && (e[0] == 's' || e[0] == 'w' || e[0] == 'W')) ? e[0] : 't';
   }();
   return v;
 }
 
-cudaError_t dispatch_fast(int dtype, int which, const SparseArgs& a, int lph, cudaStream_t st, int64_t* launches) {
+// Padded tile kernels (attn_wide.cuh; opt-in with GTE_WIDE=16|32, the default
+// is the unpadded attn_tile.cuh family): dense rows (ldq == ldv ==
+// H*dk), head chunk of 16 (bf16), 32 or 64 bytes. Lane pieces of 16 bytes
+// (default) or 32 bytes (GTE_WIDE=32). Returns the piece size in bytes and
+// sets *lpn (lanes per row), or 0 if not eligible.
+int wide_piece(int dtype, int H, int dk, int64_t ldq, int64_t ldv, std::initializer_list<const void*> ptrs,
+               int* lpn) {
+  static const int pb = [] {
+    const char* e = getenv("GTE_WIDE");
+    if (e && atoi(e) == 32) return 32;
+    if (e && atoi(e) == 16) return 16;
+    return 0;  // default: the unpadded tile kernels (faster on B200, profiles/r1c)
+  }();
+  if (pb == 0) return 0;
+  const int64_t es = (int64_t)elem_size(dtype);
+  const int64_t hb = dk * es, rowb = (int64_t)H * dk * es;
+  if (ldq != (int64_t)H * dk || ldv != ldq) return 0;
+  if (!(hb == 32 || hb == 64 || (hb == 16 && dtype == GTE_BF16))) return 0;
+  if (rowb % pb != 0) return 0;
+  const int64_t l = rowb / pb;
+  if (l != 4 && l != 8 && l != 16 && l != 32) return 0;
+  if (l * pb / 16 > 32 || hb / pb > l) return 0;
+  for (const void* q : ptrs)
+    if (q && (reinterpret_cast<uintptr_t>(q) & (pb - 1))) return 0;
+  *lpn = (int)l;
+  return pb;
+}
+
+struct WideSel {
+  int pb = 0, lpn = 0;
+};
+
+cudaError_t dispatch_fast(int dtype, int which, const SparseArgs& a, int lph, cudaStream_t st, int64_t* launches,
+                          WideSel ws = {}) {
   int lpn = 1;
   while (lpn < a.H) lpn <<= 1;
   lpn *= lph;
+  if (fast_schedule() == 't' && ws.pb) {
+    int n = 0;
+    const int hb = a.dk * (int)elem_size(dtype);
+    cudaError_t e = dtype == GTE_F32 ? launch_wide_f32(which, a, hb, ws.pb, ws.lpn, st, &n)
+                                     : launch_wide_bf16(which, a, hb, ws.pb, ws.lpn, st, &n);
+    *launches += n;
+    return e;
+  }
   if (fast_schedule() == 't') {
     int n = 0;
     cudaError_t e = dtype == GTE_F32 ? launch_tile_f32(which, a, lph, lpn, st, &n)
@@ -620,7 +663,9 @@ int gte_sparse_attn_fwd(gte_ctx* c, const gte_plan* plan, int dtype, int H, int 
     CUDA_TRY(l2_prefetch(c, {k, v}, {rows * ldq * es, rows * ldv * es}));
   }
   if (lph) {
-    CUDA_TRY(dispatch_fast(dtype, kFwd, a, lph, c->stream, &c->launches));
+    WideSel wl;
+    wl.pb = wide_piece(dtype, H, dk, ldq, ldv, {q, k, v, out}, &wl.lpn);
+    CUDA_TRY(dispatch_fast(dtype, kFwd, a, lph, c->stream, &c->launches, wl));
   } else {
     CUDA_TRY(dispatch(dtype, kFwd, a, dht, lpn, c->stream));
     c->launches += 1;
@@ -671,11 +716,13 @@ int gte_sparse_attn_bwd(gte_ctx* c, const gte_plan* plan, int dtype, int H, int 
     if (pf) {
       CUDA_TRY(l2_prefetch(c, {k, v}, {rows * ldq * es, rows * ldv * es}));
     }
-    CUDA_TRY(dispatch_fast(dtype, kBwdRows, a, lph, c->stream, &c->launches));
+    WideSel wl;
+    wl.pb = wide_piece(dtype, H, dk, ldq, ldv, {q, k, v, out, dout, dq, dk_out, dv_out}, &wl.lpn);
+    CUDA_TRY(dispatch_fast(dtype, kBwdRows, a, lph, c->stream, &c->launches, wl));
     if (pf) {
       CUDA_TRY(l2_prefetch(c, {q, dout}, {rows * ldq * es, rows * ldv * es}));
     }
-    CUDA_TRY(dispatch_fast(dtype, kBwdCols, a, lph, c->stream, &c->launches));
+    CUDA_TRY(dispatch_fast(dtype, kBwdCols, a, lph, c->stream, &c->launches, wl));
   } else {
     CUDA_TRY(dispatch(dtype, kBwdRows, a, dht, lpn, c->stream));
     CUDA_TRY(dispatch(dtype, kBwdCols, a, dht, lpn, c->stream));
