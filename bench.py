@@ -9,9 +9,12 @@ through the C ABI with pinned host buffers (H2D + D2H inside the timed region).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--dtype f32|bf16] [--impl ours|reference]
 
-N > 1 (torchrun, one rank per GPU): every rank runs its own replica of the
-sequence (weak scaling, no data-path collective); value = N*S / max-over-ranks
-step time.
+N > 1 (torchrun, one rank per GPU): the sequence-parallel layer of the
+reference (parallel.cpp:190-332): S/N token rows and H/N heads per GPU,
+Ulysses all-to-all over NCCL (csrc/sp.cu); strong scaling, value = S /
+max-over-ranks step time. --replicas instead runs N independent replicas
+(weak scaling, value = N*S / time); --sp runs the sequence-parallel path at
+N = 1 too (one-rank NCCL communicator).
 """
 from __future__ import annotations
 
@@ -72,6 +75,7 @@ def make_workload(seed=7, pattern="ecr", info=None):
     info["grid_permute_s"] = time.perf_counter() - t0
     info["diag_edge_fraction"] = P.diagonal_edge_fraction(grid)
     info["graph_E"] = int(g.nnz())
+    info["_perm_forward"] = np.asarray(perm.forward, dtype=np.int64)
     if pattern == "edge":
         return np.asarray(gp.row_offsets), np.asarray(gp.col_indices)
     bg = P.density(g)
@@ -180,18 +184,21 @@ def cpu_baseline(ro, co, sample_rows=131072, steps=3, warmup=1, threads=None):
 def cached_workload(pattern, info):
     """make_workload with a best-effort on-disk cache (same inputs -> same
     pattern; the cache only saves the ~1 min host reorder on repeat runs)."""
-    path = os.path.join(tempfile.gettempdir(), f"gte_c3_{pattern}_v1.npz")
+    path = os.path.join(tempfile.gettempdir(), f"gte_c3_{pattern}_v2.npz")
     if os.path.exists(path):
         try:
             d = np.load(path, allow_pickle=False)
             info.update(json.loads(str(d["info"])))
             info["cached"] = True
+            info["_perm_forward"] = d["perm"]
             return d["ro"], d["co"]
         except Exception:
             pass
     ro, co = make_workload(pattern=pattern, info=info)
     try:
-        np.savez(path, ro=ro, co=co, info=np.array(json.dumps(info)))
+        pf = info["_perm_forward"]
+        meta = {k: v for k, v in info.items() if not k.startswith("_")}
+        np.savez(path, ro=ro, co=co, perm=pf, info=np.array(json.dumps(meta)))
     except OSError:
         pass
     return ro, co
@@ -219,6 +226,123 @@ def run_reference_arm(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def run_sequence_parallel(args, rank, world, local, dist):
+    """N > 1: the C3 layer sequence-parallel over N GPUs, reference semantics
+    (parallel.cpp:190-332, Ulysses head split): every rank owns S/N token rows
+    (partition_sequence order) and H/N heads; seq->head all-to-all of Q, K, V
+    (NCCL send/recv over NVLink, csrc/sp.cu), attention over the whole pattern
+    for its heads, head->seq all-to-all of O; backward: all-to-all of dO,
+    attention backward, all-to-all of dQ, dK, dV, all-gather + worker-ordered
+    sum of dbias. Strong scaling: value = S / max-over-ranks step time."""
+    import torch
+
+    from paper_2407_14106_b200 import attention as A
+    from paper_2407_14106_b200 import parallel as SP
+
+    args.warmup = max(3, args.warmup)
+    info = {}
+    ro, co = cached_workload(args.pattern, info)
+    S, E = ro.shape[0] - 1, co.shape[0]
+    if H % world:
+        raise SystemExit(f"--gpus {world}: heads {H} not divisible")
+    dev = torch.device("cuda", local)
+    td = torch.float32 if args.dtype == "f32" else torch.bfloat16
+    e = 4 if args.dtype == "f32" else 2
+    ctx = A.Context.get(local)
+    plan = A.DevicePlan.from_host(ro, co, ctx)
+    if not args.no_schedule:
+        info["communities"] = plan.schedule()
+    shards = SP.partition_sequence(S, world, 1234)
+    sp = SP.SequenceParallelPlan([sh.token_ids for sh in shards], info["_perm_forward"], ctx)
+    ex = SP.NcclExchange(sp, rank, world)
+    layer = SP.UlyssesAttention.on_device(plan, sp, H, H * DH, args.dtype, ex)
+    rows = sp.rows
+    g = torch.Generator(device=dev).manual_seed(99 + rank)
+    q, k, v, do = (torch.randn((rows, H * DH), generator=g, device=dev).to(td) for _ in range(4))
+    bias = (0.3 * torch.randn(E, generator=torch.Generator(device=dev).manual_seed(7), device=dev)).float()
+    flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+
+    def step(inp=None):
+        qq, kk, vv, dd = inp or (q, k, v, do)
+        o, _ = layer.forward({rank: qq}, {rank: kk}, {rank: vv}, bias)
+        return o, layer.backward({rank: dd}, bias)
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    n0 = ctx.launches
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        for i in range(args.steps):
+            flush.zero_()
+            evs[i][0].record(stream)
+            step()
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+    launches = ctx.launches - n0
+    ms = float(np.mean([a.elapsed_time(b) for a, b in evs]))
+    t = torch.tensor([ms], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+
+    # e2e: pinned host shards in, host shards out, every step
+    pin = lambda x: x.cpu().pin_memory()  # noqa: E731
+    hq, hk, hv, hdo = pin(q), pin(k), pin(v), pin(do)
+    ho, hdq, hdk, hdv = (torch.empty(x.shape, dtype=x.dtype).pin_memory() for x in (q, q, k, v))
+    hdb = torch.empty(E, dtype=torch.float32).pin_memory()
+
+    def e2e_step():
+        dq_ = [x.to(dev, non_blocking=True) for x in (hq, hk, hv, hdo)]
+        o, (gq, gk, gv, gb) = step(tuple(dq_))
+        for h_, d_ in ((ho, o[rank]), (hdq, gq[rank]), (hdk, gk[rank]), (hdv, gv[rank]), (hdb, gb)):
+            h_.copy_(d_, non_blocking=True)
+        torch.cuda.synchronize()
+
+    for _ in range(2):
+        e2e_step()
+    dist.barrier()
+    e2e_steps = max(3, min(args.steps, 10))
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_step()
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    t = torch.tensor([e2e_s], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_s = float(t.item())
+    if rank == 0:
+        hbm, tc, peak_kind = peaks()
+        alg = algorithmic_bytes(S, E, e) / world  # per GPU: its heads' share of the unit
+        a2a = 8 * rows * H * DH * e * (world - 1) // world  # per GPU sent per step (Q,K,V,O,dO,dQ,dK,dV)
+        line = {
+            "metric": METRIC, "value": S / (ms * 1e-3), "unit": "nodes/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+            "config": {"workload": "C3 ogbn-products-shaped community graph, S=262144, GPH-slim H=8 dh=8, reorder "
+                                   "k=8 + Elastic reformation, sequence-parallel (Ulysses all-to-all over NCCL)",
+                       "S": S, "E": int(E), "heads": H, "head_dim": DH, "pattern": args.pattern,
+                       "parallelism": f"sp{world} (head-split all-to-all, reference parallel.cpp)",
+                       "rows_per_gpu": rows, "a2a_bytes_sent_per_gpu_per_step": a2a,
+                       "preprocess": {k_: v_ for k_, v_ in info.items() if not k_.startswith("_")},
+                       "l2": "flushed between timed steps (2x126MB write)"},
+            "roofline": {"bound": "hbm", "achieved": alg / (ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+                         "frac": alg / (ms * 1e-3) / 1e9 / hbm, "traffic": None, "peak_source": peak_kind,
+                         "kernel": "per-GPU step incl. all-to-all (algorithmic bytes of its H/N heads)",
+                         "algorithmic_bytes_per_step": alg},
+            "e2e": {"value": S / e2e_s, "unit": "nodes/s", "h2d_bytes_per_step": 4 * rows * H * DH * e,
+                    "d2h_bytes_per_step": 4 * rows * H * DH * e + 4 * E, "ms_per_step": e2e_s * 1e3},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    ex.close()
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -229,6 +353,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (profiling runs)")
     ap.add_argument("--no-schedule", action="store_true", help="execute rows in natural order (no community schedule)")
+    ap.add_argument("--sp", action="store_true", help="run the sequence-parallel layer even at N = 1 (NCCL, 1 rank)")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: independent replicas (weak scaling) instead of the sequence-parallel layer")
     ap.add_argument("--pattern", default="ecr", choices=["ecr", "edge"],
                     help="ecr: reorder + Elastic layout (default, the C3 config); edge: reordered graph pattern")
     args = ap.parse_args()
@@ -243,10 +370,14 @@ def main():
 
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    if world > 1 or args.sp:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29577")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local), rank=rank, world_size=world)
+        if args.sp or not args.replicas:
+            return run_sequence_parallel(args, rank, world, local, dist)
     from paper_2407_14106_b200 import attention as A
 
     args.warmup = max(3, args.warmup)
@@ -347,12 +478,13 @@ def main():
         traffic = json.load(open(prof)).get("dram_bytes_per_step")
     line = {
         "metric": METRIC, "value": world * S / (ms * 1e-3), "unit": "nodes/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak" if args.replicas else "strong", "vs_baseline": None,
         "dtype": args.dtype, "data": "synthetic",
         "config": {"workload": "C3 ogbn-products-shaped community graph (ids shuffled), S=262144, GPH-slim H=8 "
                                "dh=8, cluster reorder k=8 + Elastic reformation beta_thre=5*beta_G d_b=16",
                    "S": S, "E": int(E), "heads": H, "head_dim": DH, "pattern": args.pattern,
-                   "preprocess": info,
+                   "preprocess": {k: v for k, v in info.items() if not k.startswith("_")},
                    "parallelism": f"replicas x{world}" if world > 1 else "single",
                    "schedule": "natural" if args.no_schedule else "community (label propagation)",
                    "l2": "flushed between timed steps (2x126MB write); inputs 8x" + f"{S*H*DH*e/2**20:.0f}MB > L2"},

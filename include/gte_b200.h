@@ -204,6 +204,45 @@ int gte_check_conditions(int64_t n, int64_t nnz, const int64_t* row_off, const i
 int gte_select_mode(const int32_t* flags, int64_t epoch, int64_t dense_period, int32_t* mode, int32_t* reason);
 int gte_partition_sequence(int64_t seq_len, int64_t num_workers, uint64_t seed, int64_t* ids, int64_t* padded);
 
+/* ---- sequence parallelism (reference parallel.cpp:115-332, Ulysses
+ * head-split all-to-all) ----
+ * gte_sp: the exchange plan of P workers — token ids per worker (worker-major,
+ * P x rows, the partition_sequence order; a permutation of [0, P*rows)) and the
+ * cluster permutation's forward map (old -> execution position; null =
+ * identity). The four halves of the two exchanges (d = hidden width, H =
+ * heads for the divisibility checks of parallel.cpp:39-46, chunk = rows x d/P):
+ *   pack_seq    worker shard [rows x d]   -> send [P][rows][d/P] (chunk p = columns p*d/P..)
+ *   unpack_head recv [P][rows][d/P]       -> slice [S_pad x d/P], row of token t at perm.forward[t]
+ *   pack_head   slice [S_pad x d/P]       -> send [P][rows][d/P] (chunk p = worker p's tokens)
+ *   unpack_seq  recv [P][rows][d/P]       -> worker shard [rows x d] (chunk p -> columns p*d/P..)
+ * The exchange between them is an equal-split all-to-all: gte_comm_all_to_all
+ * (NCCL, one rank per GPU) or gte_sp_loopback (P logical workers in one
+ * process, send_all [src][dst] -> recv_all [dst][src]). */
+typedef struct gte_sp gte_sp;
+typedef struct gte_comm gte_comm;
+#define GTE_NCCL_ID_BYTES 128
+int gte_sp_create(gte_ctx* ctx, int64_t P, int64_t rows_per_worker, const int64_t* token_ids,
+                  const int64_t* perm_forward, gte_sp** out);
+int gte_sp_destroy(gte_sp* sp);
+int gte_sp_pack_seq(gte_ctx* ctx, const gte_sp* sp, int dtype, int64_t d, int64_t H, const void* shard, void* send);
+int gte_sp_unpack_head(gte_ctx* ctx, const gte_sp* sp, int dtype, int64_t d, int64_t H, const void* recv,
+                       void* slice_exec);
+int gte_sp_pack_head(gte_ctx* ctx, const gte_sp* sp, int dtype, int64_t d, int64_t H, const void* slice_exec,
+                     void* send);
+int gte_sp_unpack_seq(gte_ctx* ctx, const gte_sp* sp, int dtype, int64_t d, int64_t H, const void* recv,
+                      void* shard);
+int gte_sp_loopback(gte_ctx* ctx, const gte_sp* sp, int dtype, int64_t d, const void* send_all, void* recv_all);
+/* dbias of the distributed backward: sum of P per-worker partials [P][n] in
+ * worker order (parallel.cpp:319); dtype selects f64 or f32 accumulators */
+int gte_sp_ordered_sum(gte_ctx* ctx, int dtype, int64_t P, int64_t n, const void* parts, void* out);
+/* NCCL communicator (one rank per GPU; the id comes from rank 0's
+ * gte_nccl_unique_id, shared out of band, e.g. torch.distributed) */
+int gte_nccl_unique_id(void* id_out);
+int gte_comm_create(gte_ctx* ctx, int nranks, int rank, const void* id, gte_comm** out);
+int gte_comm_destroy(gte_comm* comm);
+int gte_comm_all_to_all(gte_comm* comm, gte_ctx* ctx, const void* send, void* recv, int64_t bytes_per_peer);
+int gte_comm_all_gather(gte_comm* comm, gte_ctx* ctx, const void* send, void* recv, int64_t bytes);
+
 #ifdef __cplusplus
 }
 #endif
