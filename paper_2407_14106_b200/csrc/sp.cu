@@ -18,6 +18,7 @@
 // Ledger (CommLedger, parallel.hpp:23-44) is exact host arithmetic in the
 // Python mirror (paper_2407_14106_b200/parallel.py).
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 #include <nccl.h>
 #include <stdint.h>
 
@@ -47,7 +48,7 @@ using namespace gte_b200;
   do {                                                                                                 \
     ncclResult_t r_ = (expr);                                                                          \
     if (r_ != ncclSuccess)                                                                             \
-      return set_error(GTE_NCCL, std::string("NCCL error: ") + ncclGetErrorString(r_) + " at " + __FILE__ + \
+      return set_error(GTE_NCCL, std::string("NCCL error: ") + nccl().GetErrorString(r_) + " at " + __FILE__ + \
                                      ":" + std::to_string(__LINE__));                                  \
   } while (0)
 
@@ -56,6 +57,58 @@ struct gte_sp {
   int32_t* d_tokens = nullptr;          // [P * rows] token ids, worker-major (partition_sequence order)
   int32_t* d_pos = nullptr;             // [P * rows] execution position perm.forward[token]
 };
+
+// NCCL is resolved at first use with dlopen("libnccl.so.2"): inside a torch
+// process that returns the NCCL torch already loaded (one NCCL per process),
+// elsewhere the system library. Linking it at build time would pin the
+// system NCCL into every process that loads libgte_b200.so first.
+namespace {
+struct NcclApi {
+  bool ok = false;
+  std::string why;
+  decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
+  decltype(&ncclCommInitRank) CommInitRank = nullptr;
+  decltype(&ncclCommDestroy) CommDestroy = nullptr;
+  decltype(&ncclGroupStart) GroupStart = nullptr;
+  decltype(&ncclGroupEnd) GroupEnd = nullptr;
+  decltype(&ncclSend) Send = nullptr;
+  decltype(&ncclRecv) Recv = nullptr;
+  decltype(&ncclAllGather) AllGather = nullptr;
+  decltype(&ncclGetErrorString) GetErrorString = nullptr;
+};
+const NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      a.why = std::string("NCCL not found: ") + dlerror();
+      return a;
+    }
+#define GTE_SYM(F) a.F = reinterpret_cast<decltype(a.F)>(dlsym(h, "nccl" #F))
+    GTE_SYM(GetUniqueId);
+    GTE_SYM(CommInitRank);
+    GTE_SYM(CommDestroy);
+    GTE_SYM(GroupStart);
+    GTE_SYM(GroupEnd);
+    GTE_SYM(Send);
+    GTE_SYM(Recv);
+    GTE_SYM(AllGather);
+    GTE_SYM(GetErrorString);
+#undef GTE_SYM
+    a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.GroupStart && a.GroupEnd && a.Send && a.Recv &&
+           a.AllGather && a.GetErrorString;
+    if (!a.ok) a.why = "NCCL library lacks a required symbol";
+    return a;
+  }();
+  return api;
+}
+}  // namespace
+
+#define NCCL_API_OR_FAIL()                                       \
+  do {                                                           \
+    if (!nccl().ok) return set_error(GTE_NCCL, nccl().why);      \
+  } while (0)
 
 struct gte_comm {
   ncclComm_t comm = nullptr;
@@ -280,8 +333,9 @@ int gte_sp_ordered_sum(gte_ctx* ctx, int dtype, int64_t P, int64_t n, const void
 
 // ---- NCCL: one rank per GPU over NVLink / NVSwitch ----
 int gte_nccl_unique_id(void* id_out) {
+  NCCL_API_OR_FAIL();
   ncclUniqueId id;
-  SNCCL(ncclGetUniqueId(&id));
+  SNCCL(nccl().GetUniqueId(&id));
   static_assert(sizeof(ncclUniqueId) == GTE_NCCL_ID_BYTES, "ncclUniqueId size");
   memcpy(id_out, &id, sizeof id);
   return GTE_OK;
@@ -290,13 +344,14 @@ int gte_nccl_unique_id(void* id_out) {
 int gte_comm_create(gte_ctx* ctx, int nranks, int rank, const void* id_in, gte_comm** out) {
   (void)ctx;
   if (nranks < 1 || rank < 0 || rank >= nranks) return set_error(GTE_CONFIG, "comm: bad rank / world size");
+  NCCL_API_OR_FAIL();
   ncclUniqueId id;
   memcpy(&id, id_in, sizeof id);
   auto* c = new gte_comm();
-  ncclResult_t r = ncclCommInitRank(&c->comm, nranks, id, rank);
+  ncclResult_t r = nccl().CommInitRank(&c->comm, nranks, id, rank);
   if (r != ncclSuccess) {
     delete c;
-    return set_error(GTE_NCCL, std::string("NCCL error: ") + ncclGetErrorString(r) + " (ncclCommInitRank)");
+    return set_error(GTE_NCCL, std::string("NCCL error: ") + nccl().GetErrorString(r) + " (ncclCommInitRank)");
   }
   c->nranks = nranks;
   c->rank = rank;
@@ -306,7 +361,7 @@ int gte_comm_create(gte_ctx* ctx, int nranks, int rank, const void* id_in, gte_c
 
 int gte_comm_destroy(gte_comm* c) {
   if (!c) return GTE_OK;
-  ncclCommDestroy(c->comm);
+  if (nccl().ok) nccl().CommDestroy(c->comm);
   delete c;
   return GTE_OK;
 }
@@ -314,18 +369,19 @@ int gte_comm_destroy(gte_comm* c) {
 int gte_comm_all_to_all(gte_comm* c, gte_ctx* ctx, const void* send, void* recv, int64_t bytes_per_peer) {
   // equal-split all-to-all: chunk p of `send` goes to rank p, chunk p of `recv` comes from rank p
   cudaStream_t st = (cudaStream_t)ctx_stream(ctx);
-  SNCCL(ncclGroupStart());
+  const NcclApi& N = nccl();
+  SNCCL(N.GroupStart());
   for (int p = 0; p < c->nranks; ++p) {
-    SNCCL(ncclSend(static_cast<const char*>(send) + p * bytes_per_peer, (size_t)bytes_per_peer, ncclUint8, p, c->comm, st));
-    SNCCL(ncclRecv(static_cast<char*>(recv) + p * bytes_per_peer, (size_t)bytes_per_peer, ncclUint8, p, c->comm, st));
+    SNCCL(N.Send(static_cast<const char*>(send) + p * bytes_per_peer, (size_t)bytes_per_peer, ncclUint8, p, c->comm, st));
+    SNCCL(N.Recv(static_cast<char*>(recv) + p * bytes_per_peer, (size_t)bytes_per_peer, ncclUint8, p, c->comm, st));
   }
-  SNCCL(ncclGroupEnd());
+  SNCCL(N.GroupEnd());
   return GTE_OK;
 }
 
 int gte_comm_all_gather(gte_comm* c, gte_ctx* ctx, const void* send, void* recv, int64_t bytes) {
   cudaStream_t st = (cudaStream_t)ctx_stream(ctx);
-  SNCCL(ncclAllGather(send, recv, (size_t)bytes, ncclUint8, c->comm, st));
+  SNCCL(nccl().AllGather(send, recv, (size_t)bytes, ncclUint8, c->comm, st));
   return GTE_OK;
 }
 
