@@ -204,6 +204,26 @@ int gte_check_conditions(int64_t n, int64_t nnz, const int64_t* row_off, const i
 int gte_select_mode(const int32_t* flags, int64_t epoch, int64_t dense_period, int32_t* mode, int32_t* reason);
 int gte_partition_sequence(int64_t seq_len, int64_t num_workers, uint64_t seed, int64_t* ids, int64_t* padded);
 
+/* ---- dense (all-pairs) attention, flash-style (reference attention.cpp:46-94,
+ * 174-239; Trainer dense epochs model.cpp:395-405) ----
+ * Rows r < s_real attend exactly the columns [0, s_real); pad rows r >= s_real
+ * attend only themselves (out = m * v_r, no score gradient). s_real = S is the
+ * reference's dense_attention. bias: [S x S] accumulate-type, shared by heads,
+ * or null; wmult: head-major [H x S x S] or null; lse [S x H] (log2 units for
+ * f32/bf16, natural log for f64); dbias [S x S] summed over heads, or null. */
+int gte_dense_attn_fwd(gte_ctx* ctx, int dtype, int64_t S, int64_t s_real, int H, int dk, int dv, const void* q,
+                       const void* k, int64_t ldq, const void* v, int64_t ldv, const void* bias, const void* wmult,
+                       void* out, void* lse);
+int gte_dense_attn_bwd(gte_ctx* ctx, int dtype, int64_t S, int64_t s_real, int H, int dk, int dv, const void* q,
+                       const void* k, int64_t ldq, const void* v, int64_t ldv, const void* out, const void* lse,
+                       const void* dout, const void* bias, const void* wmult, void* dq, void* dk_out, void* dv_out,
+                       void* dbias);
+int gte_dense_attn_fwd_host(gte_ctx* ctx, int dtype, int64_t S, int64_t s_real, int H, int dk, int dv, const void* q,
+                            const void* k, const void* v, const void* bias, const void* wmult, void* out, void* lse);
+int gte_dense_attn_bwd_host(gte_ctx* ctx, int dtype, int64_t S, int64_t s_real, int H, int dk, int dv, const void* q,
+                            const void* k, const void* v, const void* bias, const void* wmult, const void* dout,
+                            void* dq, void* dk_out, void* dv_out, void* dbias);
+
 /* ---- sequence parallelism (reference parallel.cpp:115-332, Ulysses
  * head-split all-to-all) ----
  * gte_sp: the exchange plan of P workers — token ids per worker (worker-major,

@@ -223,22 +223,12 @@ AttnGrads sparse_attention_backward(const Matrix& q, const Matrix& k, const Matr
 }
 
 namespace {
-// dense_attention over the all-pairs pattern (plans cached per S)
-const PlanHandle& dense_plan(Index s) {
-  static std::map<Index, std::unique_ptr<PlanHandle>> cache;
-  static std::mutex mu;
-  std::lock_guard<std::mutex> lk(mu);
-  auto it = cache.find(s);
-  if (it == cache.end()) it = cache.emplace(s, std::make_unique<PlanHandle>(dense_pattern(s))).first;
-  return *it->second;
-}
-
 void check_finite_matrix(const Matrix& m, const char* name) {  // attention.cpp:20-22
   if (!m.all_finite()) throw DataError(std::string("attention: non-finite ") + name);
 }
 }  // namespace
 
-// attention.cpp:46-94
+// attention.cpp:46-94 -> flash-style dense kernel (gte_dense_attn_fwd_host, f64)
 AttnResult dense_attention(const Matrix& q, const Matrix& k, const Matrix& v, const Matrix* bias,
                            const Matrix* weight_mult) {
   check_shapes(q, k, v);
@@ -254,15 +244,15 @@ AttnResult dense_attention(const Matrix& q, const Matrix& k, const Matrix& v, co
     throw ConfigError("dense_attention: weight_mult shape");
   AttnResult res;
   res.output = Matrix(s, v.cols());
-  std::vector<Real> lse;
-  run_fwd(dense_plan(s), 1, q.cols(), v.cols(), q.data(), k.data(), v.data(), bias ? bias->data() : nullptr,
-          weight_mult ? weight_mult->data() : nullptr, res.output.data(), lse, 0);
+  ck(gte_dense_attn_fwd_host(ctx(), GTE_F64, s, s, 1, static_cast<int>(q.cols()), static_cast<int>(v.cols()),
+                                  q.data(), k.data(), v.data(), bias ? bias->data() : nullptr,
+                                  weight_mult ? weight_mult->data() : nullptr, res.output.data(), nullptr));
   res.macs.score_macs = s * s * q.cols();
   res.macs.weight_macs = s * s * v.cols();
   return res;
 }
 
-// attention.cpp:174-239
+// attention.cpp:174-239 -> flash-style dense backward (gte_dense_attn_bwd_host, f64)
 AttnGrads dense_attention_backward(const Matrix& q, const Matrix& k, const Matrix& v, const Matrix* bias,
                                    const Matrix* weight_mult, const Matrix& upstream) {
   check_shapes(q, k, v);
@@ -274,16 +264,11 @@ AttnGrads dense_attention_backward(const Matrix& q, const Matrix& k, const Matri
   g.dk = Matrix(s, dk);
   g.dv = Matrix(s, dv);
   g.dbias.assign(static_cast<size_t>(s * s), 0.0);
-  const PlanHandle& plan = dense_plan(s);
-  Matrix out(s, dv);
-  std::vector<Real> lse;
-  const Real* b = bias ? bias->data() : nullptr;
-  const Real* w = weight_mult ? weight_mult->data() : nullptr;
-  run_fwd(plan, 1, dk, dv, q.data(), k.data(), v.data(), b, w, out.data(), lse, GTE_IGNORE_NONFINITE);
-  std::vector<Real> db(static_cast<size_t>(s * s) + 1, 0.0);
-  run_bwd(plan, 1, dk, dv, q.data(), k.data(), v.data(), out.data(), lse, upstream.data(), b, w, g.dq.data(),
-          g.dk.data(), g.dv.data(), db.data());
-  std::copy(db.begin(), db.begin() + s * s, g.dbias.begin());
+  if (s == 0) return g;
+  ck(gte_dense_attn_bwd_host(ctx(), GTE_F64, s, s, 1, static_cast<int>(dk), static_cast<int>(dv), q.data(),
+                                  k.data(), v.data(), bias ? bias->data() : nullptr,
+                                  weight_mult ? weight_mult->data() : nullptr, upstream.data(), g.dq.data(),
+                                  g.dk.data(), g.dv.data(), g.dbias.data()));
   return g;
 }
 

@@ -388,3 +388,117 @@ class DeviceSparseAttention:
         check(_lib.lib().gte_sparse_attn_fwd_bwd_host(
             self.plan.ctx.h, self.plan.h, self.code, self.H, self.dk, self.dv, p(q), p(k), p(v), p(dout), p(bias),
             p(out), p(dq), p(dk), p(dv), p(dbias)))
+
+
+# --------------------------------------------------------------------------
+# dense (all-pairs) attention, flash-style kernels (csrc/dense.cu)
+# --------------------------------------------------------------------------
+
+def _bind_dense():
+    L = _lib.lib()
+    if not getattr(L, "_dense_bound", False):
+        VPt, I64t, I32t = C.c_void_p, C.c_int64, C.c_int
+        L.gte_dense_attn_fwd.argtypes = [VPt, I32t, I64t, I64t, I32t, I32t, I32t, VPt, VPt, I64t, VPt, I64t, VPt, VPt,
+                                         VPt, VPt]
+        L.gte_dense_attn_bwd.argtypes = [VPt, I32t, I64t, I64t, I32t, I32t, I32t, VPt, VPt, I64t, VPt, I64t, VPt, VPt,
+                                         VPt, VPt, VPt, VPt, VPt, VPt, VPt]
+        L.gte_dense_attn_fwd_host.argtypes = [VPt, I32t, I64t, I64t, I32t, I32t, I32t, VPt, VPt, VPt, VPt, VPt, VPt,
+                                              VPt]
+        L.gte_dense_attn_bwd_host.argtypes = [VPt, I32t, I64t, I64t, I32t, I32t, I32t, VPt, VPt, VPt, VPt, VPt, VPt,
+                                              VPt, VPt, VPt, VPt]
+        L._dense_bound = True
+    return L
+
+
+def _dense_checks(q, k, v, bias, weight_mult):
+    _check_shapes(q, k, v)
+    s = q.shape[0]
+    for m, nm in ((q, "Q"), (k, "K"), (v, "V")):  # attention.cpp:20-22
+        if not np.all(np.isfinite(m)):
+            raise DataError(f"attention: non-finite {nm}")
+    if bias is not None:
+        if np.shape(bias) != (s, s):
+            raise ConfigError("dense_attention: bias shape")
+        if not np.all(np.isfinite(bias)):
+            raise DataError("attention: non-finite bias")
+    if weight_mult is not None and np.shape(weight_mult) != (s, s):
+        raise ConfigError("dense_attention: weight_mult shape")
+
+
+def dense_attention(q, k, v, bias=None, weight_mult=None, *, dtype: str = "f64") -> AttnResult:
+    """reference proj/src/attention.cpp:46-94 (bias, weight_mult: S x S or None)."""
+    q, k, v = (np.asarray(x) for x in (q, k, v))
+    _dense_checks(q, k, v, bias, weight_mult)
+    L = _bind_dense()
+    dt = _NP[dtype]
+    S, dk = q.shape
+    dv = v.shape[1]
+    qq, kk, vv, b, w = _prep(q, dt), _prep(k, dt), _prep(v, dt), _prep(bias, dt), _prep(weight_mult, dt)
+    out = np.zeros((S, dv), dt)
+    check(L.gte_dense_attn_fwd_host(Context.get().h, _lib.DTYPES[dtype], S, S, 1, dk, dv, qq.ctypes.data,
+                                    kk.ctypes.data, vv.ctypes.data, _ptr(b), _ptr(w), out.ctypes.data, None))
+    return AttnResult(out, MacCounter(S * S * dk, S * S * dv))
+
+
+def dense_attention_backward(q, k, v, bias, weight_mult, upstream, *, dtype: str = "f64") -> AttnGrads:
+    """reference proj/src/attention.cpp:174-239; dbias is S x S row-major (flattened)."""
+    q, k, v, upstream = (np.asarray(x) for x in (q, k, v, upstream))
+    _check_shapes(q, k, v)
+    S, dk = q.shape
+    dv = v.shape[1]
+    if upstream.shape != (S, dv):
+        raise ConfigError("dense_attention_backward: upstream shape mismatch")
+    L = _bind_dense()
+    dt = _NP[dtype]
+    qq, kk, vv, uu = (_prep(x, dt) for x in (q, k, v, upstream))
+    b, w = _prep(bias, dt), _prep(weight_mult, dt)
+    dq, dkk, dvv = np.zeros((S, dk), dt), np.zeros((S, dk), dt), np.zeros((S, dv), dt)
+    db = np.zeros(S * S, dt)
+    check(L.gte_dense_attn_bwd_host(Context.get().h, _lib.DTYPES[dtype], S, S, 1, dk, dv, qq.ctypes.data,
+                                    kk.ctypes.data, vv.ctypes.data, _ptr(b), _ptr(w), uu.ctypes.data, dq.ctypes.data,
+                                    dkk.ctypes.data, dvv.ctypes.data, db.ctypes.data))
+    return AttnGrads(dq, dkk, dvv, db)
+
+
+class DeviceDenseAttention:
+    """All heads of a dense sublayer on CUDA tensors (q/k [S, H*dk], v [S, H*dv]).
+    s_real < S gives the Trainer's dense epoch (model.cpp:395-405): real rows
+    attend [0, s_real), pad rows only themselves. bias [S, S] / weight_mult
+    [H, S, S] in the accumulate type, optional."""
+
+    def __init__(self, S: int, heads: int, dk: int, dv: int | None = None, dtype: str = "f32",
+                 s_real: int | None = None, ctx: Context | None = None):
+        self.S, self.H, self.dk, self.dv, self.dtype = S, heads, dk, dv or dk, dtype
+        self.s_real = S if s_real is None else s_real
+        self.ctx = ctx or Context.get()
+        self.code = _lib.DTYPES[dtype]
+
+    def forward(self, q, k, v, bias=None, weight_mult=None):
+        import torch
+
+        L = _bind_dense()
+        acc = torch.float64 if self.dtype == "f64" else torch.float32
+        out = torch.empty((self.S, self.H * self.dv), dtype=v.dtype, device=v.device)
+        lse = torch.empty((self.S, self.H), dtype=acc, device=v.device)
+        self.ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+        check(L.gte_dense_attn_fwd(self.ctx.h, self.code, self.S, self.s_real, self.H, self.dk, self.dv, q.data_ptr(),
+                                   k.data_ptr(), q.stride(0), v.data_ptr(), v.stride(0),
+                                   None if bias is None else bias.data_ptr(),
+                                   None if weight_mult is None else weight_mult.data_ptr(), out.data_ptr(),
+                                   lse.data_ptr()))
+        return out, lse
+
+    def backward(self, q, k, v, out, lse, dout, bias=None, weight_mult=None, want_dbias=False):
+        import torch
+
+        L = _bind_dense()
+        acc = torch.float64 if self.dtype == "f64" else torch.float32
+        dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+        db = torch.empty((self.S, self.S), dtype=acc, device=q.device) if want_dbias else None
+        self.ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+        check(L.gte_dense_attn_bwd(self.ctx.h, self.code, self.S, self.s_real, self.H, self.dk, self.dv, q.data_ptr(),
+                                   k.data_ptr(), q.stride(0), v.data_ptr(), v.stride(0), out.data_ptr(),
+                                   lse.data_ptr(), dout.data_ptr(), None if bias is None else bias.data_ptr(),
+                                   None if weight_mult is None else weight_mult.data_ptr(), dq.data_ptr(),
+                                   dk.data_ptr(), dv.data_ptr(), None if db is None else db.data_ptr()))
+        return dq, dk, dv, db
