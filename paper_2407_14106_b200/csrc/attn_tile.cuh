@@ -46,8 +46,18 @@ constexpr int kTileWarps = kTileThreads / 32;
 #endif
 constexpr int kTileRows = GTE_TILE_ROWS;  // rows (columns) per tile, <= kTileThreads
 constexpr int kTileCap = GTE_TILE_CAP;    // staged edges per tile (32 KB of ids + biases at 4096)
-constexpr int kTilePad = 8;       // padding slots after the staged edges (>= EPL)
+constexpr int kTilePad = 16;      // padding slots after the staged edges (>= EPL)
 constexpr int kHubDegree = 1024;  // longer rows/columns go to the hub kernels
+#ifndef GTE_TILE_EPL
+#define GTE_TILE_EPL 4
+#endif
+#ifndef GTE_TILE_MINB
+#define GTE_TILE_MINB 4
+#endif
+#ifndef GTE_TILE_MINB_COLS
+#define GTE_TILE_MINB_COLS 3
+#endif
+constexpr int kTileEpl = GTE_TILE_EPL;  // edges per slot per step
 
 struct TileMeta {
   int row[kTileRows];      // row (column) id
@@ -177,7 +187,7 @@ __device__ __forceinline__ void tile_own_rows(const TileMeta& mt, int nrows, con
 // ---------------------------------------------------------------------------
 // Forward: O, LSE (log2 units).
 template <typename T, int LPH, int LPN, int EPL, bool WM>
-__global__ void __launch_bounds__(kTileThreads, 4) tile_fwd_kernel(SparseArgs p) {
+__global__ void __launch_bounds__(kTileThreads, GTE_TILE_MINB) tile_fwd_kernel(SparseArgs p) {
   using P = Piece<T>;
   using M = SoftmaxMath<float>;
   constexpr int VW = P::N;
@@ -296,7 +306,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) tile_fwd_kernel(SparseArgs p)
 // CSR pass of the backward: delta, dQ, dbias (summed over heads). Writes the
 // packed (lse, delta) pair per (row, head) for the CSC pass.
 template <typename T, int LPH, int LPN, int EPL, bool WM>
-__global__ void __launch_bounds__(kTileThreads, 4) tile_bwd_rows_kernel(SparseArgs p) {
+__global__ void __launch_bounds__(kTileThreads, GTE_TILE_MINB) tile_bwd_rows_kernel(SparseArgs p) {
   using P = Piece<T>;
   using M = SoftmaxMath<float>;
   constexpr int VW = P::N;
@@ -402,7 +412,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) tile_bwd_rows_kernel(SparseAr
 // ---------------------------------------------------------------------------
 // CSC pass of the backward: dK, dV per column, no atomics.
 template <typename T, int LPH, int LPN, int EPL, bool WM>
-__global__ void __launch_bounds__(kTileThreads, 3) tile_bwd_cols_kernel(SparseArgs p) {
+__global__ void __launch_bounds__(kTileThreads, GTE_TILE_MINB_COLS) tile_bwd_cols_kernel(SparseArgs p) {
   using P = Piece<T>;
   using M = SoftmaxMath<float>;
   constexpr int VW = P::N;

@@ -49,8 +49,8 @@ cudaError_t launch_tile_one(int which, const SparseArgs& a, cudaStream_t st, int
 
 template <typename T, int LPH, int LPN>
 cudaError_t launch_tile_wm(int which, const SparseArgs& a, cudaStream_t st, int* launches) {
-  return a.wmult ? launch_tile_one<T, LPH, LPN, 4, true>(which, a, st, launches)
-                 : launch_tile_one<T, LPH, LPN, 4, false>(which, a, st, launches);
+  return a.wmult ? launch_tile_one<T, LPH, LPN, kTileEpl, true>(which, a, st, launches)
+                 : launch_tile_one<T, LPH, LPN, kTileEpl, false>(which, a, st, launches);
 }
 
 template <typename T, int LPH>
