@@ -137,6 +137,13 @@ struct gte_plan {
   int n_tiles = 0, n_hubs = 0, n_tiles_c = 0, n_hubs_c = 0;
   bool scheduled = false;
   int64_t communities = 0;
+  // halo of the tile kernels (build_halo): per tile the most-referenced
+  // neighbour rows (staged in shared memory once per tile) and the staged
+  // neighbour ids with halo members encoded as ~slot, per pass
+  int halo_cap = 0;          // rows per tile the halo was built for (0: none)
+  int32_t* halo = nullptr;   // one allocation: off, ids, off_c, ids_c, xcols, xrows
+  const int32_t *halo_off = nullptr, *halo_ids = nullptr, *halo_off_c = nullptr, *halo_ids_c = nullptr;
+  const int32_t *xcols = nullptr, *xrows = nullptr;
 };
 
 namespace {
@@ -289,10 +296,108 @@ int build_exec(gte_plan* p, const int64_t* order) {
   p->order_c = where[1][0];
   p->tiles_c = where[1][1];
   p->hubs_c = where[1][2];
+  cudaFree(p->halo);
+  p->halo = nullptr;
+  p->halo_cap = 0;
   p->n_tiles = (int)ps[0].tiles.size() - 1;
   p->n_hubs = (int)ps[0].hubs.size();
   p->n_tiles_c = (int)ps[1].tiles.size() - 1;
   p->n_hubs_c = (int)ps[1].hubs.size();
+  return GTE_OK;
+}
+
+// Halo of the tile kernels: for every tile of both passes, the (at most
+// `cap`) neighbour rows its edges reference most often (>= 2 references, ties
+// to the smaller id), listed per tile; the staged neighbour-id arrays of both
+// passes with halo members replaced by ~slot (negative). An execution aid
+// only: the kernels read the same K/V (Q/dO/LSE) values from shared memory
+// instead of L2, so outputs are bit-identical with or without it.
+int build_halo(gte_plan* p, int cap) {
+  const int64_t n = p->rows, m = p->nnz;
+  cudaStream_t st = p->ctx->stream;
+  std::vector<int32_t> rp(n + 1), cp(n + 1), ci(m > 0 ? m : 1), cr(m > 0 ? m : 1);
+  std::vector<int32_t> order(n > 0 ? n : 1), tiles(p->n_tiles + 1), order_c(n > 0 ? n : 1), tiles_c(p->n_tiles_c + 1);
+  CUDA_TRY(cudaMemcpyAsync(rp.data(), p->row_ptr, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(cp.data(), p->col_ptr, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost, st));
+  if (m) {
+    CUDA_TRY(cudaMemcpyAsync(ci.data(), p->cols, sizeof(int32_t) * m, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(cr.data(), p->csc_row, sizeof(int32_t) * m, cudaMemcpyDeviceToHost, st));
+  }
+  CUDA_TRY(cudaMemcpyAsync(tiles.data(), p->tiles, sizeof(int32_t) * (p->n_tiles + 1), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(tiles_c.data(), p->tiles_c, sizeof(int32_t) * (p->n_tiles_c + 1), cudaMemcpyDeviceToHost, st));
+  if (p->n_tiles > 0 && tiles[p->n_tiles] > 0)
+    CUDA_TRY(cudaMemcpyAsync(order.data(), p->order, sizeof(int32_t) * tiles[p->n_tiles], cudaMemcpyDeviceToHost, st));
+  if (p->n_tiles_c > 0 && tiles_c[p->n_tiles_c] > 0)
+    CUDA_TRY(cudaMemcpyAsync(order_c.data(), p->order_c, sizeof(int32_t) * tiles_c[p->n_tiles_c], cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  struct Out {
+    std::vector<int32_t> off, ids, x;
+  } out[2];
+  std::vector<int32_t> cnt(n > 0 ? n : 1, 0), slot(n > 0 ? n : 1, -1);
+  for (int pass = 0; pass < 2; ++pass) {
+    const std::vector<int32_t>& ptr = pass == 0 ? rp : cp;
+    const std::vector<int32_t>& nb = pass == 0 ? ci : cr;
+    const std::vector<int32_t>& ord = pass == 0 ? order : order_c;
+    const std::vector<int32_t>& tl = pass == 0 ? tiles : tiles_c;
+    const int nt = pass == 0 ? p->n_tiles : p->n_tiles_c;
+    Out& O = out[pass];
+    O.x.assign(nb.begin(), nb.begin() + (m > 0 ? m : 1));
+    O.off.push_back(0);
+    std::vector<int32_t> seen;
+    for (int t = 0; t < nt; ++t) {
+      seen.clear();
+      for (int x = tl[t]; x < tl[t + 1]; ++x) {
+        const int32_t r = ord[x];
+        for (int32_t e = ptr[r]; e < ptr[r + 1]; ++e) {
+          const int32_t j = nb[e];
+          if (cnt[j]++ == 0) seen.push_back(j);
+        }
+      }
+      std::vector<int32_t> cand;
+      for (int32_t j : seen)
+        if (cnt[j] >= 2) cand.push_back(j);
+      const size_t k = std::min<size_t>(cand.size(), (size_t)cap);
+      std::partial_sort(cand.begin(), cand.begin() + k, cand.end(), [&](int32_t a, int32_t b) {
+        return cnt[a] != cnt[b] ? cnt[a] > cnt[b] : a < b;
+      });
+      for (size_t s2 = 0; s2 < k; ++s2) {
+        slot[cand[s2]] = (int32_t)s2;
+        O.ids.push_back(cand[s2]);
+      }
+      O.off.push_back((int32_t)O.ids.size());
+      for (int x = tl[t]; x < tl[t + 1]; ++x) {
+        const int32_t r = ord[x];
+        for (int32_t e = ptr[r]; e < ptr[r + 1]; ++e)
+          if (slot[nb[e]] >= 0) O.x[e] = ~slot[nb[e]];
+      }
+      for (size_t s2 = 0; s2 < k; ++s2) slot[cand[s2]] = -1;
+      for (int32_t j : seen) cnt[j] = 0;
+    }
+  }
+  size_t total = 0;
+  for (auto& O : out) total += O.off.size() + O.ids.size() + O.x.size();
+  cudaFree(p->halo);
+  p->halo = nullptr;
+  CUDA_TRY(cudaMalloc(&p->halo, sizeof(int32_t) * (total + 1)));
+  int32_t* cur = p->halo;
+  const int32_t* where[2][3];
+  for (int pass = 0; pass < 2; ++pass) {
+    std::vector<int32_t>* v[3] = {&out[pass].off, &out[pass].ids, &out[pass].x};
+    for (int a = 0; a < 3; ++a) {
+      where[pass][a] = cur;
+      if (!v[a]->empty())
+        CUDA_TRY(cudaMemcpyAsync(cur, v[a]->data(), sizeof(int32_t) * v[a]->size(), cudaMemcpyHostToDevice, st));
+      cur += v[a]->size();
+    }
+  }
+  CUDA_TRY(cudaStreamSynchronize(st));
+  p->halo_off = where[0][0];
+  p->halo_ids = where[0][1];
+  p->xcols = where[0][2];
+  p->halo_off_c = where[1][0];
+  p->halo_ids_c = where[1][1];
+  p->xrows = where[1][2];
+  p->halo_cap = cap;
   return GTE_OK;
 }
 
@@ -305,6 +410,7 @@ void free_plan(gte_plan* p) {
   cudaFree(p->csc_eid);
   cudaFree(p->unref);
   cudaFree(p->exec);
+  cudaFree(p->halo);
   delete p;
 }
 
@@ -338,6 +444,51 @@ int fast_lph(int dtype, int64_t S, int H, int dk, int dv, int64_t ldq, int64_t l
   for (const void* q : ptrs)
     if (q && (reinterpret_cast<uintptr_t>(q) & 15)) return 0;
   return lph;
+}
+
+// Halo staging of the tile kernels (opt-in, GTE_HALO=1; measured slower on
+// B200 — generic loads + selects add ~25% instructions and the halo halves
+// occupancy, profiles/r1c/ab_variants.txt): cap rows per tile
+// so that the halo of the CSC pass (Q, dO rows + (lse, delta)) fits
+// kHaloBudget. Built lazily per plan and row width (a per-pattern cache,
+// like the CSC view).
+bool halo_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("GTE_HALO");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+int halo_cap_for(int dtype, int H, int dk) {
+  static const int budget = [] {
+    const char* e = getenv("GTE_HALO_BUDGET");  // bytes per CTA (A/B experiments)
+    return e ? atoi(e) : kHaloBudget;
+  }();
+  const int rowb = H * dk * (int)elem_size(dtype);
+  int cap = budget / (2 * rowb + 8 * H);
+  return cap > 192 ? 192 : cap;
+}
+
+char fast_schedule();
+
+int use_halo(const gte_plan* plan, SparseArgs& a, int dtype, int H, int dk) {
+  if (!halo_enabled() || fast_schedule() != 't') return GTE_OK;
+  const int cap = halo_cap_for(dtype, H, dk);
+  if (cap < 16) return GTE_OK;
+  gte_plan* p = const_cast<gte_plan*>(plan);
+  if (p->halo_cap != cap) {
+    int rc = build_halo(p, cap);
+    if (rc) return rc;
+  }
+  a.halo_cap = p->halo_cap;
+  a.halo_off = p->halo_off;
+  a.halo_ids = p->halo_ids;
+  a.xcols = p->xcols;
+  a.halo_off_c = p->halo_off_c;
+  a.halo_ids_c = p->halo_ids_c;
+  a.xrows = p->xrows;
+  return GTE_OK;
 }
 
 bool prefetch_enabled() {
@@ -665,6 +816,10 @@ int gte_sparse_attn_fwd(gte_ctx* c, const gte_plan* plan, int dtype, int H, int 
   if (lph) {
     WideSel wl;
     wl.pb = wide_piece(dtype, H, dk, ldq, ldv, {q, k, v, out}, &wl.lpn);
+    if (!wl.pb) {
+      rc = use_halo(plan, a, dtype, H, dk);
+      if (rc) return rc;
+    }
     CUDA_TRY(dispatch_fast(dtype, kFwd, a, lph, c->stream, &c->launches, wl));
   } else {
     CUDA_TRY(dispatch(dtype, kFwd, a, dht, lpn, c->stream));
@@ -718,6 +873,10 @@ int gte_sparse_attn_bwd(gte_ctx* c, const gte_plan* plan, int dtype, int H, int 
     }
     WideSel wl;
     wl.pb = wide_piece(dtype, H, dk, ldq, ldv, {q, k, v, out, dout, dq, dk_out, dv_out}, &wl.lpn);
+    if (!wl.pb) {
+      rc = use_halo(plan, a, dtype, H, dk);
+      if (rc) return rc;
+    }
     CUDA_TRY(dispatch_fast(dtype, kBwdRows, a, lph, c->stream, &c->launches, wl));
     if (pf) {
       CUDA_TRY(l2_prefetch(c, {q, dout}, {rows * ldq * es, rows * ldv * es}));

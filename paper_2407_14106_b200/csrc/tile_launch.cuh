@@ -3,6 +3,9 @@
 // rows/columns), each only if non-empty. Returns the number of launches.
 #pragma once
 
+#include <utility>
+#include <vector>
+
 #include "attn_launch.cuh"
 #include "attn_tile.cuh"
 
@@ -10,28 +13,43 @@ namespace gte_b200 {
 
 template <typename K>
 cudaError_t tile_go(K kernel, int grid, size_t smem, const SparseArgs& a, cudaStream_t st) {
-  static bool configured = false;  // per kernel instantiation
-  if (!configured && smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
+  // dynamic smem above 48 KB needs an opt-in per kernel (per instantiation
+  // and per size: the attribute is set once for the largest size asked)
+  static thread_local std::vector<std::pair<const void*, size_t>> done;
+  if (smem > 48 * 1024) {
+    bool ok = false;
+    for (auto& d : done)
+      if (d.first == reinterpret_cast<const void*>(kernel) && d.second >= smem) ok = true;
+    if (!ok) {
+      cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      done.emplace_back(reinterpret_cast<const void*>(kernel), smem);
+    }
   }
   kernel<<<(unsigned)grid, kTileThreads, smem, st>>>(a);
   return cudaGetLastError();
 }
 
+template <typename T, int LPH, int LPN, int EPL, bool WM, bool HALO>
+cudaError_t launch_tile_halo(int which, const SparseArgs& a, cudaStream_t st) {
+  const int rowb = a.H * a.dk * (int)sizeof(T);
+  const size_t smem = tile_smem_bytes() + (HALO ? halo_bytes(a.halo_cap, rowb, a.H) : 0);
+  const int nt = which == kBwdCols ? a.n_tiles_c : a.n_tiles;
+  switch (which) {
+    case kFwd: return tile_go(tile_fwd_kernel<T, LPH, LPN, EPL, WM, HALO>, nt, smem, a, st);
+    case kBwdRows: return tile_go(tile_bwd_rows_kernel<T, LPH, LPN, EPL, WM, HALO>, nt, smem, a, st);
+    default: return tile_go(tile_bwd_cols_kernel<T, LPH, LPN, EPL, WM, HALO>, nt, smem, a, st);
+  }
+}
+
 template <typename T, int LPH, int LPN, int EPL, bool WM>
 cudaError_t launch_tile_one(int which, const SparseArgs& a, cudaStream_t st, int* launches) {
-  const size_t smem = tile_smem_bytes();
   cudaError_t e = cudaSuccess;
   const int nt = which == kBwdCols ? a.n_tiles_c : a.n_tiles;
   const int nh = which == kBwdCols ? a.n_hubs_c : a.n_hubs;
   if (nt > 0) {
-    switch (which) {
-      case kFwd: e = tile_go(tile_fwd_kernel<T, LPH, LPN, EPL, WM>, nt, smem, a, st); break;
-      case kBwdRows: e = tile_go(tile_bwd_rows_kernel<T, LPH, LPN, EPL, WM>, nt, smem, a, st); break;
-      default: e = tile_go(tile_bwd_cols_kernel<T, LPH, LPN, EPL, WM>, nt, smem, a, st); break;
-    }
+    e = a.halo_cap > 0 ? launch_tile_halo<T, LPH, LPN, EPL, WM, true>(which, a, st)
+                       : launch_tile_halo<T, LPH, LPN, EPL, WM, false>(which, a, st);
     if (e != cudaSuccess) return e;
     ++*launches;
   }
