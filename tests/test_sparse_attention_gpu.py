@@ -286,10 +286,11 @@ def test_wide_kernels_mixed_degrees(cuda, orc, dtype, H, dh, wm):
 
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
-@pytest.mark.parametrize("variant", ["16", "32"])
+@pytest.mark.parametrize("variant", ["W16", "W32", "HALO"])
 def test_padded_kernels_match_tile_kernels(cuda, dtype, variant):
-    """The opt-in padded kernels (GTE_WIDE=16|32, attn_wide.cuh) against the
-    default tile kernels on the mixed-degree graph (empty, degree-1..9 rows),
+    """The opt-in kernel variants (GTE_WIDE=16|32: padded kernels of
+    attn_wide.cuh; GTE_HALO=1: shared-memory halo of the tile kernels) against
+    the default tile kernels on the mixed-degree graph (empty, degree-1..9 rows),
     with a dropout mask: same scores (same dot order), outputs equal up to
     accumulation-order rounding; degree-1 rows exact in both."""
     import os
@@ -305,9 +306,10 @@ def test_padded_kernels_match_tile_kernels(cuda, dtype, variant):
     )
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outs = []
-    for wide in (variant, "0"):
-        path = os.path.join("/tmp", f"wide_cmp_{dtype}_{wide}.npz")
-        subprocess.run([sys.executable, "-c", code, path], check=True, cwd=root, env=dict(os.environ, GTE_WIDE=wide))
+    envs = {"W16": {"GTE_WIDE": "16"}, "W32": {"GTE_WIDE": "32"}, "HALO": {"GTE_HALO": "1"}}[variant]
+    for tag, extra in ((variant, envs), ("base", {"GTE_WIDE": "0", "GTE_HALO": "0"})):
+        path = os.path.join("/tmp", f"wide_cmp_{dtype}_{tag}.npz")
+        subprocess.run([sys.executable, "-c", code, path], check=True, cwd=root, env=dict(os.environ, **extra))
         outs.append(np.load(path))
     a, b = outs
     fa, fb = np.isfinite(a["lse"]), np.isfinite(b["lse"])
