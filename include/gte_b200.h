@@ -262,6 +262,19 @@ int gte_comm_create(gte_ctx* ctx, int nranks, int rank, const void* id, gte_comm
 int gte_comm_destroy(gte_comm* comm);
 int gte_comm_all_to_all(gte_comm* comm, gte_ctx* ctx, const void* send, void* recv, int64_t bytes_per_peer);
 int gte_comm_all_gather(gte_comm* comm, gte_ctx* ctx, const void* send, void* recv, int64_t bytes);
+/* variable all-to-all: per-peer byte offsets and counts (0 = no message) */
+int gte_comm_all_to_allv(gte_comm* comm, gte_ctx* ctx, const void* send, const int64_t* send_off,
+                         const int64_t* send_bytes, void* recv, const int64_t* recv_off, const int64_t* recv_bytes);
+/* ---- cluster-halo sequence parallelism ("Mode H") ----
+ * Each GPU owns a contiguous range of rows (all heads) and runs the attention
+ * kernels on a local plan over [own rows | halo rows]; the halo exchange moves
+ * K/V rows of remote neighbours in (gather -> all_to_allv straight into the
+ * halo tail) and the dK/dV partials of halo rows back to their owners
+ * (all_to_allv -> scatter-add, peers in rank order). */
+int gte_rows_gather(gte_ctx* ctx, int dtype, int64_t n, const int32_t* idx, const void* src, int64_t ld, int64_t w,
+                    void* dst);
+int gte_rows_scatter_add(gte_ctx* ctx, int dtype, int64_t n, const int32_t* idx, const void* src, int64_t w,
+                         void* dst, int64_t ld);
 
 #ifdef __cplusplus
 }

@@ -17,6 +17,7 @@
 //
 // Ledger (CommLedger, parallel.hpp:23-44) is exact host arithmetic in the
 // Python mirror (paper_2407_14106_b200/parallel.py).
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
@@ -179,6 +180,28 @@ __global__ void ordered_sum_kernel(const A* __restrict__ parts, A* __restrict__ 
   }
 }
 
+// Cluster-halo exchange (Mode H): rows picked by an index list into a
+// contiguous send block, and received partial rows added into their owner
+// rows (one source at a time, rows unique per source: no atomics).
+template <typename U>
+__global__ void gather_rows_kernel(const U* __restrict__ src, int64_t ld, const int32_t* __restrict__ idx, int64_t n,
+                                   int64_t nu, U* __restrict__ dst) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n * nu; x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = x / nu, c = x % nu;
+    dst[x] = src[(int64_t)__ldg(idx + r) * ld + c];
+  }
+}
+
+template <typename T, typename A>
+__global__ void scatter_add_rows_kernel(const T* __restrict__ src, const int32_t* __restrict__ idx, int64_t n,
+                                        int64_t w, T* __restrict__ dst, int64_t ld) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n * w; x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = x / w, c = x % w;
+    T* d = dst + (int64_t)__ldg(idx + r) * ld + c;
+    *d = T(A(*d) + A(src[x]));
+  }
+}
+
 int unit_bytes(int64_t chunk_row_bytes, std::initializer_list<const void*> ptrs) {
   for (int u : {16, 8, 4, 2, 1}) {
     if (chunk_row_bytes % u) continue;
@@ -331,6 +354,55 @@ int gte_sp_ordered_sum(gte_ctx* ctx, int dtype, int64_t P, int64_t n, const void
   return GTE_OK;
 }
 
+int gte_rows_gather(gte_ctx* ctx, int dtype, int64_t n, const int32_t* idx, const void* src, int64_t ld, int64_t w,
+                    void* dst) {
+  // dst[r][0..w) = src[idx[r]][0..w), elements of `dtype`; dst dense (ld = w)
+  if (n < 0 || w < 0 || ld < w) return set_error(GTE_CONFIG, "rows_gather: bad sizes");
+  if (n == 0 || w == 0) return GTE_OK;
+  const int64_t es = (int64_t)esize(dtype), rb = w * es;
+  int ub = 16;
+  while (ub > 1 && (rb % ub || (ld * es) % ub || reinterpret_cast<uintptr_t>(src) % ub ||
+                    reinterpret_cast<uintptr_t>(dst) % ub))
+    ub >>= 1;
+  const int64_t nu = rb / ub, ldu = ld * es / ub;
+  cudaStream_t st = (cudaStream_t)ctx_stream(ctx);
+  const unsigned g = blocks_for(n * nu);
+  switch (ub) {
+    case 16: gather_rows_kernel<uint4><<<g, 256, 0, st>>>((const uint4*)src, ldu, idx, n, nu, (uint4*)dst); break;
+    case 8: gather_rows_kernel<uint2><<<g, 256, 0, st>>>((const uint2*)src, ldu, idx, n, nu, (uint2*)dst); break;
+    case 4: gather_rows_kernel<uint32_t><<<g, 256, 0, st>>>((const uint32_t*)src, ldu, idx, n, nu, (uint32_t*)dst); break;
+    case 2: gather_rows_kernel<uint16_t><<<g, 256, 0, st>>>((const uint16_t*)src, ldu, idx, n, nu, (uint16_t*)dst); break;
+    default: gather_rows_kernel<uint8_t><<<g, 256, 0, st>>>((const uint8_t*)src, ldu, idx, n, nu, (uint8_t*)dst); break;
+  }
+  ctx_launch_counter(ctx) += 1;
+  SCUDA(cudaGetLastError());
+  return GTE_OK;
+}
+
+int gte_rows_scatter_add(gte_ctx* ctx, int dtype, int64_t n, const int32_t* idx, const void* src, int64_t w,
+                         void* dst, int64_t ld) {
+  // dst[idx[r]][0..w) += src[r][0..w) (accumulated in f32 for bf16); idx unique
+  if (n < 0 || w < 0 || ld < w) return set_error(GTE_CONFIG, "rows_scatter_add: bad sizes");
+  if (n == 0 || w == 0) return GTE_OK;
+  cudaStream_t st = (cudaStream_t)ctx_stream(ctx);
+  const unsigned g = blocks_for(n * w);
+  switch (dtype) {
+    case GTE_F64:
+      scatter_add_rows_kernel<double, double><<<g, 256, 0, st>>>((const double*)src, idx, n, w, (double*)dst, ld);
+      break;
+    case GTE_F32:
+      scatter_add_rows_kernel<float, float><<<g, 256, 0, st>>>((const float*)src, idx, n, w, (float*)dst, ld);
+      break;
+    default:
+      scatter_add_rows_kernel<__nv_bfloat16, float><<<g, 256, 0, st>>>((const __nv_bfloat16*)src, idx, n, w,
+                                                                        (__nv_bfloat16*)dst, ld);
+      break;
+  }
+  ctx_launch_counter(ctx) += 1;
+  SCUDA(cudaGetLastError());
+  return GTE_OK;
+}
+
 // ---- NCCL: one rank per GPU over NVLink / NVSwitch ----
 int gte_nccl_unique_id(void* id_out) {
   NCCL_API_OR_FAIL();
@@ -374,6 +446,22 @@ int gte_comm_all_to_all(gte_comm* c, gte_ctx* ctx, const void* send, void* recv,
   for (int p = 0; p < c->nranks; ++p) {
     SNCCL(N.Send(static_cast<const char*>(send) + p * bytes_per_peer, (size_t)bytes_per_peer, ncclUint8, p, c->comm, st));
     SNCCL(N.Recv(static_cast<char*>(recv) + p * bytes_per_peer, (size_t)bytes_per_peer, ncclUint8, p, c->comm, st));
+  }
+  SNCCL(N.GroupEnd());
+  return GTE_OK;
+}
+
+int gte_comm_all_to_allv(gte_comm* c, gte_ctx* ctx, const void* send, const int64_t* send_off,
+                         const int64_t* send_bytes, void* recv, const int64_t* recv_off, const int64_t* recv_bytes) {
+  // variable all-to-all (byte offsets / counts per peer); zero-byte pairs skipped
+  cudaStream_t st = (cudaStream_t)ctx_stream(ctx);
+  const NcclApi& N = nccl();
+  SNCCL(N.GroupStart());
+  for (int p = 0; p < c->nranks; ++p) {
+    if (send_bytes[p] > 0)
+      SNCCL(N.Send(static_cast<const char*>(send) + send_off[p], (size_t)send_bytes[p], ncclUint8, p, c->comm, st));
+    if (recv_bytes[p] > 0)
+      SNCCL(N.Recv(static_cast<char*>(recv) + recv_off[p], (size_t)recv_bytes[p], ncclUint8, p, c->comm, st));
   }
   SNCCL(N.GroupEnd());
   return GTE_OK;

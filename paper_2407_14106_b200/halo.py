@@ -1,0 +1,277 @@
+"""Cluster-halo sequence parallelism ("Mode H") for the
+sparse attention layer.
+
+The reference parallelises a layer by splitting heads (the Ulysses
+all-to-all of parallel.cpp, mirrored in parallel.py). For the *sparse* layer
+that moves ~S·d·e bytes per GPU per exchange — as much as the kernel itself
+reads. After the cluster-aware reorder (partition.cpp:413-433) the pattern is
+near block-diagonal over the k clusters, so here each GPU owns a contiguous
+range of rows (a cluster when P = k) with *all* heads and exchanges only the
+rows its edges reach in other ranges:
+
+  forward   gather own K/V rows each peer needs -> all_to_allv straight into
+            the halo tail of the local K/V buffers [own | halo] -> the same
+            sparse kernels on the local plan (own rows' edges, columns
+            renumbered into [own | halo]; halo rows have no edges)
+  backward  same kernels: dQ of own rows and dbias of own edges are complete;
+            dK/dV of halo rows are partial sums of this rank's edges -> sent
+            back to their owners (all_to_allv) and added to the owners' rows
+            in rank order (gte_rows_scatter_add; unique rows per source, no
+            atomics)
+
+The math per pair is the reference's (sparse_attention / _backward, the
+attention.cpp:96-320 semantics); only the summation order of dK/dV over
+ranks differs from a single GPU. The bias/dbias of a rank are the contiguous
+slice of the global pattern's edges that its rows own.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import ConfigError, check
+from .attention import Context, DevicePlan, DeviceSparseAttention
+
+VP, I64, I32 = C.c_void_p, C.c_int64, C.c_int
+
+
+def _bind():
+    L = _lib.lib()
+    if not getattr(L, "_halo_bound", False):
+        L.gte_rows_gather.argtypes = [VP, I32, I64, VP, VP, I64, I64, VP]
+        L.gte_rows_scatter_add.argtypes = [VP, I32, I64, VP, VP, I64, VP, I64]
+        L.gte_comm_all_to_allv.argtypes = [VP, VP, VP, VP, VP, VP, VP, VP]
+        L._halo_bound = True
+    return L
+
+
+def row_ranges(S: int, P: int) -> np.ndarray:
+    """Near-equal contiguous ranges, first S % P get one more
+    (cluster_boundaries, partition.cpp:495-500)."""
+    base, extra = divmod(S, P)
+    sizes = np.full(P, base, dtype=np.int64)
+    sizes[:extra] += 1
+    return np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+
+
+@dataclass
+class RankHalo:
+    """One rank's share of the pattern and its exchange lists."""
+    rank: int
+    lo: int
+    hi: int
+    n_own: int
+    halo_ids: np.ndarray     # global ids of halo rows (sorted: by owner, then id)
+    recv_counts: np.ndarray  # [P] halo rows received from each peer
+    send_idx: list           # [P] local own-row indices each peer needs (ascending global id)
+    local_ro: np.ndarray     # CSR over [own | halo] rows (halo rows empty)
+    local_co: np.ndarray
+    e_lo: int                # own rows' edges are [e_lo, e_hi) of the global CSR
+    e_hi: int
+
+    @property
+    def n_ext(self) -> int:
+        return self.n_own + int(self.halo_ids.shape[0])
+
+    def boundary_rows(self) -> tuple[int, int]:
+        """(rows received, rows sent) per exchange: the Mode H ledger."""
+        return int(self.recv_counts.sum()), int(sum(len(s) for s in self.send_idx))
+
+
+def build_halo_plan(row_offsets, cols, P: int) -> list[RankHalo]:
+    """Host planner (numpy, O(E)) for all P ranks; every rank can run it on the
+    replicated pattern, so no index lists travel."""
+    ro = np.asarray(row_offsets, dtype=np.int64)
+    co = np.asarray(cols, dtype=np.int64)
+    S = ro.shape[0] - 1
+    if P < 1 or P > S:
+        raise ConfigError("halo: worker count must lie in [1, S]")
+    b = row_ranges(S, P)
+    owner_of = np.repeat(np.arange(P), np.diff(b))
+    halos = []
+    for p in range(P):
+        lo, hi = int(b[p]), int(b[p + 1])
+        e_lo, e_hi = int(ro[lo]), int(ro[hi])
+        c = co[e_lo:e_hi]
+        remote = np.unique(c[(c < lo) | (c >= hi)])  # sorted by id == by owner then id
+        halos.append((lo, hi, e_lo, e_hi, remote))
+    plans = []
+    for p in range(P):
+        lo, hi, e_lo, e_hi, remote = halos[p]
+        n_own = hi - lo
+        recv_counts = np.bincount(owner_of[remote], minlength=P).astype(np.int64) if remote.size else np.zeros(P, np.int64)
+        send_idx = []
+        for q in range(P):
+            rq = halos[q][4]
+            mine = rq[(rq >= lo) & (rq < hi)] if q != p else rq[:0]
+            send_idx.append((mine - lo).astype(np.int32))
+        c = co[e_lo:e_hi]
+        own = (c >= lo) & (c < hi)
+        lc = np.empty_like(c)
+        lc[own] = c[own] - lo
+        lc[~own] = n_own + np.searchsorted(remote, c[~own])
+        n_ext = n_own + remote.shape[0]
+        lro = np.empty(n_ext + 1, dtype=np.int64)
+        lro[: n_own + 1] = ro[lo:hi + 1] - e_lo
+        lro[n_own + 1:] = e_hi - e_lo
+        plans.append(RankHalo(p, lo, hi, n_own, remote, recv_counts, send_idx, lro, lc, e_lo, e_hi))
+    return plans
+
+
+class HaloLoopback:
+    """All P ranks in one process on one GPU: the all_to_allv is a set of
+    device copies between the ranks' buffers (the reference's own execution
+    model of logical workers)."""
+
+    def __init__(self, P: int):
+        self.P = P
+
+    def exchange(self, sends: dict, recvs: dict, send_counts: dict, recv_counts: dict, row_elems: int):
+        """sends[p]: [sum_q send_counts[p][q], w] blocks in peer order; recvs[p]: destination
+        [sum_q recv_counts[p][q], w] in peer order. Copies block (p -> q)."""
+        for q in range(self.P):
+            off_q = 0
+            for p in range(self.P):
+                n = int(recv_counts[q][p])
+                if n:
+                    off_p = int(np.sum(send_counts[p][:q]))
+                    recvs[q][off_q:off_q + n].copy_(sends[p][off_p:off_p + n])
+                off_q += n
+
+
+class HaloNccl:
+    """One rank per GPU: gte_comm_all_to_allv over the NCCL communicator of a
+    parallel.NcclExchange (which owns the id broadcast)."""
+
+    def __init__(self, comm_exchange, rank: int, ctx: Context):
+        self.cx, self.rank, self.ctx = comm_exchange, rank, ctx
+
+    def exchange(self, sends: dict, recvs: dict, send_counts: dict, recv_counts: dict, row_elems: int):
+        p = self.rank
+        x, y = sends[p], recvs[p]
+        es = x.element_size() * row_elems
+        sc = np.asarray(send_counts[p], dtype=np.int64) * es
+        rc = np.asarray(recv_counts[p], dtype=np.int64) * es
+        so = np.concatenate([[0], np.cumsum(sc)[:-1]]).astype(np.int64)
+        ro_ = np.concatenate([[0], np.cumsum(rc)[:-1]]).astype(np.int64)
+        check(_bind().gte_comm_all_to_allv(self.cx.h, self.ctx.h, x.data_ptr(), so.ctypes.data, sc.ctypes.data,
+                                           y.data_ptr(), ro_.ctypes.data, rc.ctypes.data))
+
+
+class HaloAttention:
+    """The sparse attention layer over P ranks with a cluster-halo exchange.
+    `ranks` are the RankHalo plans this process holds (all P for the loopback,
+    one for NCCL). Shards: own rows [n_own, H*dh] per rank (CUDA tensors)."""
+
+    def __init__(self, ranks: list[RankHalo], P: int, heads: int, dh: int, dtype: str, exchange, ctx=None,
+                 schedule: bool = True):
+        self.ranks, self.P, self.H, self.dh, self.dtype, self.x = ranks, P, heads, dh, dtype, exchange
+        self.ctx = ctx or Context.get(0)
+        self.d = heads * dh
+        self.plans, self.att, self.idx = {}, {}, {}
+        import torch
+
+        for r in ranks:
+            plan = DevicePlan.from_host(r.local_ro, r.local_co, self.ctx)
+            if schedule:
+                plan.schedule()
+            self.plans[r.rank] = plan
+            self.att[r.rank] = DeviceSparseAttention(plan, heads, dh, dh, dtype)
+            cat = np.concatenate(r.send_idx) if r.send_idx else np.zeros(0, np.int32)
+            self.idx[r.rank] = torch.tensor(cat.astype(np.int32), device="cuda")
+        self._send_counts = {r.rank: [len(s) for s in r.send_idx] for r in ranks}
+        self._recv_counts = {r.rank: list(r.recv_counts) for r in ranks}
+        if len(ranks) == P:  # loopback: every rank's counts are local
+            self._all_send = self._send_counts
+            self._all_recv = self._recv_counts
+        self.cache = {}
+
+    def _ext(self, r: RankHalo, own):
+        import torch
+
+        t = torch.empty((r.n_ext, self.d), dtype=own.dtype, device=own.device)
+        t[: r.n_own].copy_(own)
+        return t
+
+    def _halo_in(self, tensors: dict):
+        """Fill the halo tails of ext buffers {rank: ext} with the owners' rows."""
+        import torch
+
+        L = _bind()
+        code = _lib.DTYPES[self.dtype]
+        sends, recvs = {}, {}
+        for r in self.ranks:
+            ext = tensors[r.rank]
+            n = int(self.idx[r.rank].numel())
+            buf = torch.empty((max(n, 1), self.d), dtype=ext.dtype, device=ext.device)
+            if n:
+                check(L.gte_rows_gather(self.ctx.h, code, n, self.idx[r.rank].data_ptr(), ext.data_ptr(), self.d,
+                                        self.d, buf.data_ptr()))
+            sends[r.rank] = buf
+            recvs[r.rank] = ext[r.n_own:]
+        self.x.exchange(sends, recvs, self._all_send_counts(), self._all_recv_counts(), self.d)
+
+    def _halo_back(self, tensors: dict):
+        """Send the halo rows' partial sums to their owners and add them."""
+        import torch
+
+        L = _bind()
+        code = _lib.DTYPES[self.dtype]
+        sends, recvs = {}, {}
+        for r in self.ranks:
+            ext = tensors[r.rank]
+            sends[r.rank] = ext[r.n_own:]
+            n = int(self.idx[r.rank].numel())
+            recvs[r.rank] = torch.empty((max(n, 1), self.d), dtype=ext.dtype, device=ext.device)
+        # reverse direction: what rank p received from q, it now sends back to q
+        self.x.exchange(sends, recvs, self._all_recv_counts(), self._all_send_counts(), self.d)
+        for r in self.ranks:
+            # one launch per source peer, in rank order: rows are unique within
+            # a peer's block (no atomics) and the summation order is fixed
+            off = 0
+            idx, rv = self.idx[r.rank], recvs[r.rank]
+            for n in self._send_counts[r.rank]:
+                if n:
+                    check(L.gte_rows_scatter_add(self.ctx.h, code, n, idx[off:].data_ptr(), rv[off:].data_ptr(),
+                                                 self.d, tensors[r.rank].data_ptr(), self.d))
+                off += n
+
+    def _all_send_counts(self):
+        return getattr(self, "_all_send", self._send_counts)
+
+    def _all_recv_counts(self):
+        return getattr(self, "_all_recv", self._recv_counts)
+
+    def forward(self, q: dict, k: dict, v: dict, bias=None):
+        """bias: the global pattern's [E] (each rank uses its edges' slice)."""
+        kx = {r.rank: self._ext(r, k[r.rank]) for r in self.ranks}
+        vx = {r.rank: self._ext(r, v[r.rank]) for r in self.ranks}
+        self._halo_in(kx)
+        self._halo_in(vx)
+        out = {}
+        for r in self.ranks:
+            qx = self._ext(r, q[r.rank])
+            b = None if bias is None else bias[r.e_lo:r.e_hi]
+            o, lse = self.att[r.rank].forward(qx, kx[r.rank], vx[r.rank], b)
+            self.cache[r.rank] = (qx, kx[r.rank], vx[r.rank], o, lse, b)
+            out[r.rank] = o[: r.n_own]
+        return out
+
+    def backward(self, dout: dict):
+        """Returns {rank: (dq_own, dk_own, dv_own, dbias_own_edges)}."""
+        import torch
+
+        gq, gk, gv, gb = {}, {}, {}, {}
+        for r in self.ranks:
+            qx, kx, vx, o, lse, b = self.cache[r.rank]
+            dox = torch.zeros_like(o)
+            dox[: r.n_own].copy_(dout[r.rank])
+            dq, dk, dv, db = self.att[r.rank].backward(qx, kx, vx, o, lse, dox, b)
+            gq[r.rank], gk[r.rank], gv[r.rank], gb[r.rank] = dq, dk, dv, db
+        self._halo_back(gk)
+        self._halo_back(gv)
+        return {r.rank: (gq[r.rank][: r.n_own], gk[r.rank][: r.n_own], gv[r.rank][: r.n_own],
+                         gb[r.rank][: r.e_hi - r.e_lo]) for r in self.ranks}

@@ -1,0 +1,104 @@
+"""Cluster-halo sequence parallelism on the device (halo.py + csrc/sp.cu
+gather / scatter-add / all_to_allv): P logical ranks on one GPU (loopback
+exchange) against the single-GPU layer and the oracle; the NCCL all_to_allv
+on a one-rank communicator."""
+import numpy as np
+import pytest
+
+from conftest import rel_err
+from oracle import CSR
+
+from paper_2407_14106_b200 import attention as A
+from paper_2407_14106_b200.datagen import community_graph
+from paper_2407_14106_b200.halo import HaloAttention, HaloLoopback, build_halo_plan
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"f64": 1e-12, "f32": 1e-5, "bf16": 1e-2}
+
+
+def _run(ro, co, P, H, dh, dtype, seed=0):
+    import torch
+
+    td = {"f64": torch.float64, "f32": torch.float32, "bf16": torch.bfloat16}[dtype]
+    acc = torch.float64 if dtype == "f64" else torch.float32
+    S, E = ro.shape[0] - 1, co.shape[0]
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    q, k, v, up = (torch.randn((S, H * dh), generator=g, device="cuda").to(td) for _ in range(4))
+    bias = (0.3 * torch.randn(E, generator=g, device="cuda")).to(acc)
+    plans = build_halo_plan(ro, co, P)
+    layer = HaloAttention(plans, P, H, dh, dtype, HaloLoopback(P))
+    sl = lambda t, r: t[r.lo:r.hi].contiguous()  # noqa: E731
+    out = layer.forward({r.rank: sl(q, r) for r in plans}, {r.rank: sl(k, r) for r in plans},
+                        {r.rank: sl(v, r) for r in plans}, bias)
+    grads = layer.backward({r.rank: sl(up, r) for r in plans})
+    torch.cuda.synchronize()
+    cat = lambda d: torch.cat([d[r.rank] for r in plans]).double().cpu().numpy()  # noqa: E731
+    res = dict(out=cat(out), dq=cat({p: grads[p][0] for p in grads}), dk=cat({p: grads[p][1] for p in grads}),
+               dv=cat({p: grads[p][2] for p in grads}), db=cat({p: grads[p][3] for p in grads}))
+    # single-GPU reference path
+    plan = A.DevicePlan.from_host(ro, co)
+    att = A.DeviceSparseAttention(plan, H, dh, dh, dtype)
+    o1, lse1 = att.forward(q, k, v, bias)
+    dq1, dk1, dv1, db1 = att.backward(q, k, v, o1, lse1, up, bias)
+    torch.cuda.synchronize()
+    f = lambda t: t.double().cpu().numpy()  # noqa: E731
+    one = dict(out=f(o1), dq=f(dq1), dk=f(dk1), dv=f(dv1), db=f(db1)[:E])
+    inputs = dict(q=f(q), k=f(k), v=f(v), up=f(up), bias=f(bias))
+    return res, one, inputs, plans
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_halo_matches_single_gpu(cuda, dtype, P):
+    ro, co = community_graph(20000, 12.0, community=256, seed=P, shuffle=False)
+    res, one, _, plans = _run(ro, co, P, 8, 8, dtype, seed=P)
+    for nm in ("out", "dq", "dk", "dv", "db"):
+        e = rel_err(res[nm], one[nm])
+        assert max(e) <= TOL[dtype], (nm, e)
+    if dtype == "f32":  # rows whose columns are all local: identical arithmetic
+        assert np.array_equal(res["out"][:10], res["out"][:10])
+    recv = sum(r.boundary_rows()[0] for r in plans)
+    assert recv > 0
+
+
+def test_halo_f64_vs_oracle(cuda, orc):
+    ro, co = community_graph(3000, 9.0, community=64, seed=11, shuffle=True)
+    res, _, x, _ = _run(ro, co, 3, 2, 4, "f64", seed=3)
+    g = CSR(3000, ro, co)
+    db = np.zeros(co.shape[0])
+    for h in range(2):
+        sl = slice(h * 4, (h + 1) * 4)
+        w = orc.sparse_fwd(x["q"][:, sl], x["k"][:, sl], x["v"][:, sl], g, x["bias"])
+        assert max(rel_err(res["out"][:, sl], w)) <= 1e-12
+        a, b, c, e = orc.sparse_bwd(x["q"][:, sl], x["k"][:, sl], x["v"][:, sl], g, x["bias"], None, x["up"][:, sl])
+        for got, want in ((res["dq"][:, sl], a), (res["dk"][:, sl], b), (res["dv"][:, sl], c)):
+            assert max(rel_err(got, want)) <= 1e-12
+        db += e
+    assert max(rel_err(res["db"], db)) <= 1e-12
+
+
+def test_all_to_allv_single_rank(cuda):
+    """gte_comm_all_to_allv on a one-rank NCCL communicator: a local copy."""
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2407_14106_b200 import parallel as SP
+    from paper_2407_14106_b200.halo import HaloNccl
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29563")
+    if not dist.is_initialized():
+        dist.init_process_group("gloo", rank=0, world_size=1)
+    ctx = A.Context.get(0)
+    sp = SP.SequenceParallelPlan([np.arange(8, dtype=np.int64)], None, ctx)
+    nx = SP.NcclExchange(sp, 0, 1)
+    hx = HaloNccl(nx, 0, ctx)
+    x = torch.arange(40, dtype=torch.float32, device="cuda").reshape(10, 4)
+    y = torch.zeros_like(x)
+    hx.exchange({0: x}, {0: y}, {0: [10]}, {0: [10]}, 4)
+    torch.cuda.synchronize()
+    assert torch.equal(x, y)
+    nx.close()
