@@ -252,22 +252,37 @@ def run_sequence_parallel(args, rank, world, local, dist):
     plan = A.DevicePlan.from_host(ro, co, ctx)
     if not args.no_schedule:
         info["communities"] = plan.schedule()
-    shards = SP.partition_sequence(S, world, 1234)
-    sp = SP.SequenceParallelPlan([sh.token_ids for sh in shards], info["_perm_forward"], ctx)
-    ex = SP.NcclExchange(sp, rank, world)
-    layer = SP.UlyssesAttention.on_device(plan, sp, H, H * DH, args.dtype, ex)
-    rows = sp.rows
+    bias = (0.3 * torch.randn(E, generator=torch.Generator(device=dev).manual_seed(7), device=dev)).float()
+    if args.sp_mode == "ulysses":
+        shards = SP.partition_sequence(S, world, 1234)
+        sp = SP.SequenceParallelPlan([sh.token_ids for sh in shards], info["_perm_forward"], ctx)
+        ex = SP.NcclExchange(sp, rank, world)
+        layer = SP.UlyssesAttention.on_device(plan, sp, H, H * DH, args.dtype, ex)
+        rows = sp.rows
+        halo_rows = None
+    else:
+        from paper_2407_14106_b200 import halo as HL
+
+        hp = HL.build_halo_plan(ro, co, world)
+        ex = SP.NcclExchange(None, rank, world, ctx=ctx)
+        layer = HL.HaloAttention([hp[rank]], world, H, DH, args.dtype, HL.HaloNccl(ex, rank, ctx), ctx,
+                                 schedule=not args.no_schedule)
+        rows = hp[rank].n_own
+        halo_rows = [list(r.boundary_rows()) for r in hp]
     g = torch.Generator(device=dev).manual_seed(99 + rank)
     q, k, v, do = (torch.randn((rows, H * DH), generator=g, device=dev).to(td) for _ in range(4))
-    bias = (0.3 * torch.randn(E, generator=torch.Generator(device=dev).manual_seed(7), device=dev)).float()
     flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
 
     def step(inp=None):
         qq, kk, vv, dd = inp or (q, k, v, do)
-        o, _ = layer.forward({rank: qq}, {rank: kk}, {rank: vv}, bias)
-        return o, layer.backward({rank: dd}, bias)
+        if args.sp_mode == "ulysses":
+            o, _ = layer.forward({rank: qq}, {rank: kk}, {rank: vv}, bias)
+            return o, layer.backward({rank: dd}, bias)
+        o = layer.forward({rank: qq}, {rank: kk}, {rank: vv}, bias)
+        gq, gk, gv, gb = layer.backward({rank: dd})[rank]
+        return o, ({rank: gq}, {rank: gk}, {rank: gv}, gb)
 
     for _ in range(args.warmup):
         flush.zero_()
@@ -294,11 +309,14 @@ def run_sequence_parallel(args, rank, world, local, dist):
     pin = lambda x: x.cpu().pin_memory()  # noqa: E731
     hq, hk, hv, hdo = pin(q), pin(k), pin(v), pin(do)
     ho, hdq, hdk, hdv = (torch.empty(x.shape, dtype=x.dtype).pin_memory() for x in (q, q, k, v))
-    hdb = torch.empty(E, dtype=torch.float32).pin_memory()
+    hdb = None
 
     def e2e_step():
+        nonlocal hdb
         dq_ = [x.to(dev, non_blocking=True) for x in (hq, hk, hv, hdo)]
         o, (gq, gk, gv, gb) = step(tuple(dq_))
+        if hdb is None:
+            hdb = torch.empty(gb.shape, dtype=gb.dtype).pin_memory()
         for h_, d_ in ((ho, o[rank]), (hdq, gq[rank]), (hdk, gk[rank]), (hdv, gv[rank]), (hdb, gb)):
             h_.copy_(d_, non_blocking=True)
         torch.cuda.synchronize()
@@ -317,15 +335,21 @@ def run_sequence_parallel(args, rank, world, local, dist):
     if rank == 0:
         hbm, tc, peak_kind = peaks()
         alg = algorithmic_bytes(S, E, e) / world  # per GPU: its heads' share of the unit
-        a2a = 8 * rows * H * DH * e * (world - 1) // world  # per GPU sent per step (Q,K,V,O,dO,dQ,dK,dV)
+        if args.sp_mode == "ulysses":
+            a2a = 8 * rows * H * DH * e * (world - 1) // world  # per GPU sent per step (Q,K,V,O,dO,dQ,dK,dV)
+        else:  # K, V halo rows in; dK, dV halo partials back (rank 0's view)
+            a2a = 2 * (halo_rows[0][0] + halo_rows[0][1]) * H * DH * e
         line = {
             "metric": METRIC, "value": S / (ms * 1e-3), "unit": "nodes/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
             "config": {"workload": "C3 ogbn-products-shaped community graph, S=262144, GPH-slim H=8 dh=8, reorder "
-                                   "k=8 + Elastic reformation, sequence-parallel (Ulysses all-to-all over NCCL)",
+                                   "k=8 + Elastic reformation, sequence-parallel over NCCL ("
+                                   + ("Ulysses head-split all-to-all" if args.sp_mode == "ulysses"
+                                      else "cluster-halo exchange") + ")",
+                       "sp_mode": args.sp_mode, "halo_rows_recv_sent_per_rank": halo_rows,
                        "S": S, "E": int(E), "heads": H, "head_dim": DH, "pattern": args.pattern,
-                       "parallelism": f"sp{world} (head-split all-to-all, reference parallel.cpp)",
+                       "parallelism": f"sp{world} ({args.sp_mode})",
                        "rows_per_gpu": rows, "a2a_bytes_sent_per_gpu_per_step": a2a,
                        "preprocess": {k_: v_ for k_, v_ in info.items() if not k_.startswith("_")},
                        "l2": "flushed between timed steps (2x126MB write)"},
@@ -334,7 +358,7 @@ def run_sequence_parallel(args, rank, world, local, dist):
                          "kernel": "per-GPU step incl. all-to-all (algorithmic bytes of its H/N heads)",
                          "algorithmic_bytes_per_step": alg},
             "e2e": {"value": S / e2e_s, "unit": "nodes/s", "h2d_bytes_per_step": 4 * rows * H * DH * e,
-                    "d2h_bytes_per_step": 4 * rows * H * DH * e + 4 * E, "ms_per_step": e2e_s * 1e3},
+                    "d2h_bytes_per_step": 4 * rows * H * DH * e + 4 * int(hdb.numel()), "ms_per_step": e2e_s * 1e3},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
         }
@@ -354,6 +378,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (profiling runs)")
     ap.add_argument("--no-schedule", action="store_true", help="execute rows in natural order (no community schedule)")
     ap.add_argument("--sp", action="store_true", help="run the sequence-parallel layer even at N = 1 (NCCL, 1 rank)")
+    ap.add_argument("--sp-mode", default="halo", choices=["halo", "ulysses"],
+                    help="N > 1: cluster-halo row exchange (default) or the reference's Ulysses head split")
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: independent replicas (weak scaling) instead of the sequence-parallel layer")
     ap.add_argument("--pattern", default="ecr", choices=["ecr", "edge"],

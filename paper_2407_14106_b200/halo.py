@@ -189,11 +189,17 @@ class HaloAttention:
             self._all_recv = self._recv_counts
         self.cache = {}
 
-    def _ext(self, r: RankHalo, own):
+    def _ext(self, r: RankHalo, own, zero_tail: bool = False):
+        """[own | halo] buffer. Tails that no exchange fills (Q, dO) are zeroed:
+        the kernels' padding slots may read any row of the local index space."""
         import torch
 
+        if r.n_ext == r.n_own:
+            return own.contiguous()
         t = torch.empty((r.n_ext, self.d), dtype=own.dtype, device=own.device)
         t[: r.n_own].copy_(own)
+        if zero_tail:
+            t[r.n_own:].zero_()
         return t
 
     def _halo_in(self, tensors: dict):
@@ -253,7 +259,7 @@ class HaloAttention:
         self._halo_in(vx)
         out = {}
         for r in self.ranks:
-            qx = self._ext(r, q[r.rank])
+            qx = self._ext(r, q[r.rank], zero_tail=True)
             b = None if bias is None else bias[r.e_lo:r.e_hi]
             o, lse = self.att[r.rank].forward(qx, kx[r.rank], vx[r.rank], b)
             self.cache[r.rank] = (qx, kx[r.rank], vx[r.rank], o, lse, b)
@@ -267,8 +273,7 @@ class HaloAttention:
         gq, gk, gv, gb = {}, {}, {}, {}
         for r in self.ranks:
             qx, kx, vx, o, lse, b = self.cache[r.rank]
-            dox = torch.zeros_like(o)
-            dox[: r.n_own].copy_(dout[r.rank])
+            dox = self._ext(r, dout[r.rank], zero_tail=True)
             dq, dk, dv, db = self.att[r.rank].backward(qx, kx, vx, o, lse, dox, b)
             gq[r.rank], gk[r.rank], gv[r.rank], gb[r.rank] = dq, dk, dv, db
         self._halo_back(gk)

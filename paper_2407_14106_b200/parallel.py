@@ -203,14 +203,15 @@ class NcclExchange:
     """One rank per GPU: rank r is worker r. The 128-byte NCCL id travels over
     an existing torch.distributed group (plumbing); the data path is NCCL."""
 
-    def __init__(self, sp: SequenceParallelPlan, rank: int, world: int, group=None):
+    def __init__(self, sp: SequenceParallelPlan | None, rank: int, world: int, group=None, ctx: Context | None = None):
         import torch
         import torch.distributed as dist
 
         L = _bind()
-        if sp.P != world:
+        if sp is not None and sp.P != world:
             raise ConfigError("comm: worker count must equal the world size")
         self.sp, self.rank, self.local = sp, rank, [rank]
+        self.ctx = sp.ctx if sp is not None else (ctx or Context.get(0))
         idb = (C.c_uint8 * 128)()
         if rank == 0:
             check(L.gte_nccl_unique_id(C.cast(idb, VP)))
@@ -221,7 +222,7 @@ class NcclExchange:
         raw = bytes(t.cpu().tolist())
         idb = (C.c_uint8 * 128).from_buffer_copy(raw)
         h = VP()
-        check(L.gte_comm_create(sp.ctx.h, world, rank, C.cast(idb, VP), C.byref(h)))
+        check(L.gte_comm_create(self.ctx.h, world, rank, C.cast(idb, VP), C.byref(h)))
         self.h = h
 
     def all_to_all(self, send: dict, dtype: str, d: int) -> dict:
