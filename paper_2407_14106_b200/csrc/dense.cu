@@ -26,12 +26,16 @@
 #include <stdint.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
 #include "../../include/gte_b200.h"
 
 namespace gte_b200 {
+cudaError_t launch_dense_tc_fwd(int64_t S, int64_t s_real, int H, int dk, int dv, const void* q, const void* k,
+                                int64_t ldq, const void* v, int64_t ldv, const void* bias, const void* wmult,
+                                void* out, void* lse, cudaStream_t st);
 int set_error(int code, const std::string& msg);
 int64_t& ctx_launch_counter(gte_ctx* c);
 void* ctx_stream(gte_ctx* c);
@@ -434,7 +438,15 @@ int gte_dense_attn_fwd(gte_ctx* ctx, int dtype, int64_t S, int64_t s_real, int H
   a.S = S, a.s_real = s_real, a.H = H, a.dk = dk, a.dv = dv, a.ldq = ldq, a.ldv = ldv;
   a.q = q, a.k = k, a.v = v, a.bias = bias, a.wmult = wmult, a.out = out, a.lse = lse;
   a.scale = 1.0 / std::sqrt((double)dk);
-  DCUDA(launch(dtype, 0, a, (cudaStream_t)ctx_stream(ctx)));
+  static const bool tc = [] {  // bf16: both GEMMs on tcgen05 (dense_tc.cu); GTE_DENSE_TC=0 -> CUDA cores
+    const char* e = getenv("GTE_DENSE_TC");
+    return !(e && e[0] == '0');
+  }();
+  if (dtype == GTE_BF16 && tc)
+    DCUDA(launch_dense_tc_fwd(S, s_real, H, dk, dv, q, k, ldq, v, ldv, bias, wmult, out, lse,
+                              (cudaStream_t)ctx_stream(ctx)));
+  else
+    DCUDA(launch(dtype, 0, a, (cudaStream_t)ctx_stream(ctx)));
   ctx_launch_counter(ctx) += 1;
   return GTE_OK;
 }

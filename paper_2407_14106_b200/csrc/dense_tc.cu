@@ -1,0 +1,338 @@
+// Dense attention forward on the 5th-generation tensor cores (bf16): the
+// flash-style dense layer of csrc/dense.cu with both GEMMs on tcgen05.
+//
+// CTA = 128 query rows x one head, 4 warps; thread t owns TMEM lane / row t.
+// Per block of 128 keys:
+//   1. stage K [128 keys x DKP] and V^T [DVP x 128 keys] (bf16) into shared
+//      memory in the canonical K-major, no-swizzle UMMA layout (8-row x
+//      16-byte core matrices; LBO = 128 B between the two 8-element k halves
+//      of a core-matrix pair, SBO between 8-row groups);
+//   2. one elected thread issues S = Q K^T (M = 128, N = 128, K = DKP, bf16
+//      -> f32 in TMEM columns [0, 128)) and commits to an mbarrier;
+//   3. every thread tcgen05.ld's its row of S (4 x 32 columns), runs the
+//      online-softmax update in registers (log2 domain, ex2), writes P (bf16)
+//      into shared memory (A operand, K-major);
+//   4. the elected thread issues O_blk = P V (M = 128, N = DVP, K = 128) into
+//      TMEM columns [0, DVP) (S is already in registers) and commits;
+//   5. every thread tcgen05.ld's its O_blk row: acc = acc * corr + O_blk.
+// The epilogue normalises, writes O (bf16) and LSE (f32, log2 units) exactly
+// like dense.cu, so the CUDA-core backward (dense.cu) consumes it unchanged.
+// Pad rows (>= s_real) attend only themselves (out = m * v_r exactly).
+//
+// At head_dim 8 the tensor cores are far from the bound: 128 exps per row per
+// key block (MUFU) dominate, 2 MMAs per block do the 4*dh flops per pair.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cmath>
+#include <string>
+
+#include "../../include/gte_b200.h"
+
+namespace gte_b200 {
+int set_error(int code, const std::string& msg);
+int64_t& ctx_launch_counter(gte_ctx* c);
+void* ctx_stream(gte_ctx* c);
+}  // namespace gte_b200
+
+using namespace gte_b200;
+
+namespace {
+
+constexpr int kM = 128;  // query rows per CTA (= TMEM lanes = threads)
+constexpr int kN = 128;  // keys per block
+
+struct TcArgs {
+  int64_t S, s_real;
+  int H, dk, dv;
+  int64_t ldq, ldv;
+  const __nv_bfloat16 *q, *k, *v;
+  const float* bias;   // [S*S] or null
+  const float* wmult;  // [H*S*S] or null
+  __nv_bfloat16* out;
+  float* lse;
+  float scale_l;  // log2(e) / sqrt(dk)
+};
+
+// byte offset of element (r, kk) in a canonical K-major no-swizzle tile whose
+// rows hold KW bf16 elements: core matrices of 8 rows x 8 elements (128 B)
+__device__ __forceinline__ uint32_t canon(int r, int kk, int KW) {
+  return (uint32_t)((r >> 3) * (KW * 16) + (kk >> 3) * 128 + (r & 7) * 16 + (kk & 7) * 2);
+}
+
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
+  // base offset 0, lbo mode 0, layout type 0 = SWIZZLE_NONE
+  return d;
+}
+
+__host__ __device__ constexpr uint32_t instr_desc(int M, int N) {
+  return (1u << 4)                     // D format f32
+         | (1u << 7) | (1u << 10)      // A, B bf16
+         | ((uint32_t)(N >> 3) << 17)  // N
+         | ((uint32_t)(M >> 4) << 24); // M; A, B K-major
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(b) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(b),
+      "r"(phase)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_before_sync() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_after_sync() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+template <int DKP, int DVP>
+__global__ void __launch_bounds__(kM) dense_tc_fwd_kernel(TcArgs a) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  unsigned char* Qs = smem;                       // [128 x DKP]
+  unsigned char* Ks = Qs + kM * DKP * 2;          // [128 x DKP]
+  unsigned char* Vt = Ks + kN * DKP * 2;          // [DVP x 128]
+  unsigned char* Ps = Vt + DVP * kN * 2;          // [128 x 128]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(Ps + kM * kN * 2);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
+
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int h = blockIdx.y;
+  const int64_t r0 = (int64_t)blockIdx.x * kM;
+  const int64_t row = r0 + tid;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(
+        (uint32_t)__cvta_generic_to_shared(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // stage Q (rows >= s_real: zeros; they are handled by the epilogue)
+  for (int x = tid; x < kM * DKP; x += kM) {
+    const int r = x / DKP, kk = x % DKP;
+    const int64_t gr = r0 + r;
+    __nv_bfloat16 val = __float2bfloat16(0.f);
+    if (gr < a.s_real && kk < a.dk) val = a.q[gr * a.ldq + (int64_t)h * a.dk + kk];
+    *reinterpret_cast<__nv_bfloat16*>(Qs + canon(r, kk, DKP)) = val;
+  }
+  tc_before_sync();
+  __syncthreads();
+  tc_after_sync();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_row = tmem + ((uint32_t)(warp * 32) << 16);  // this warp's 32 lanes
+  const uint32_t sQ = (uint32_t)__cvta_generic_to_shared(Qs), sK = (uint32_t)__cvta_generic_to_shared(Ks);
+  const uint32_t sV = (uint32_t)__cvta_generic_to_shared(Vt), sP = (uint32_t)__cvta_generic_to_shared(Ps);
+  constexpr uint32_t kIdS = instr_desc(kM, kN), kIdO = instr_desc(kM, DVP);
+
+  float m = -INFINITY, l = 0.f, acc[DVP];
+#pragma unroll
+  for (int t = 0; t < DVP; ++t) acc[t] = 0.f;
+  uint32_t phase = 0;
+  const bool real = row < a.s_real;
+
+  for (int64_t c0 = 0; c0 < a.s_real; c0 += kN) {
+    const int n = (int)(a.s_real - c0 < kN ? a.s_real - c0 : kN);
+    // 1. stage K block and V^T block
+    for (int x = tid; x < kN * DKP; x += kM) {
+      const int c = x / DKP, kk = x % DKP;
+      __nv_bfloat16 val = __float2bfloat16(0.f);
+      if (c < n && kk < a.dk) val = a.k[(c0 + c) * a.ldq + (int64_t)h * a.dk + kk];
+      *reinterpret_cast<__nv_bfloat16*>(Ks + canon(c, kk, DKP)) = val;
+    }
+    for (int x = tid; x < kN * DVP; x += kM) {
+      const int c = x / DVP, t = x % DVP;
+      __nv_bfloat16 val = __float2bfloat16(0.f);
+      if (c < n && t < a.dv) val = a.v[(c0 + c) * a.ldv + (int64_t)h * a.dv + t];
+      *reinterpret_cast<__nv_bfloat16*>(Vt + canon(t, c, kN)) = val;
+    }
+    fence_async_smem();
+    tc_before_sync();
+    __syncthreads();
+    tc_after_sync();
+    // 2. S = Q K^T
+    if (tid == 0) {
+#pragma unroll
+      for (int kc = 0; kc < DKP / 16; ++kc)
+        mma_bf16(tmem, smem_desc(sQ + kc * 256, 128, DKP * 16), smem_desc(sK + kc * 256, 128, DKP * 16), kIdS,
+                 kc > 0);
+      mma_commit(bar);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    tc_after_sync();
+    // 3. online softmax on this thread's row
+    float s[kN];
+#pragma unroll
+    for (int q4 = 0; q4 < kN / 32; ++q4) {
+      float v32[32];
+      tmem_ld32(t_row + q4 * 32, v32);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) s[q4 * 32 + i] = v32[i];
+    }
+    float mx = -INFINITY;
+#pragma unroll
+    for (int c = 0; c < kN; ++c) {
+      float x = s[c] * a.scale_l;
+      if (a.bias && real && c < n) x = fmaf(a.bias[row * a.S + c0 + c], 1.4426950408889634f, x);
+      s[c] = c < n ? x : -INFINITY;
+      mx = fmaxf(mx, s[c]);
+    }
+    const float mn = fmaxf(m, mx);
+    const float corr = exp2f(m - mn);
+    l *= corr;
+#pragma unroll
+    for (int c8 = 0; c8 < kN / 8; ++c8) {
+      uint32_t w[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int c = c8 * 8 + 2 * i;
+        float p0 = exp2f(s[c] - mn), p1 = exp2f(s[c + 1] - mn);
+        l += p0 + p1;
+        if (a.wmult && real) {
+          const float* wr = a.wmult + ((int64_t)h * a.S + row) * a.S + c0;
+          p0 = c < n ? p0 * wr[c] : 0.f;
+          p1 = c + 1 < n ? p1 * wr[c + 1] : 0.f;
+        }
+        __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
+        w[i] = *reinterpret_cast<uint32_t*>(&b2);
+      }
+      *reinterpret_cast<uint4*>(Ps + canon(tid, c8 * 8, kN)) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+    m = mn;
+    fence_async_smem();
+    tc_before_sync();
+    __syncthreads();
+    tc_after_sync();
+    // 4. O_blk = P V into TMEM columns [0, DVP)
+    if (tid == 0) {
+#pragma unroll
+      for (int kc = 0; kc < kN / 16; ++kc)
+        mma_bf16(tmem, smem_desc(sP + kc * 256, 128, kN * 16), smem_desc(sV + kc * 256, 128, kN * 16), kIdO, kc > 0);
+      mma_commit(bar);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    tc_after_sync();
+    // 5. acc = acc * corr + O_blk
+#pragma unroll
+    for (int q4 = 0; q4 < (DVP + 31) / 32; ++q4) {
+      float v32[32];
+      tmem_ld32(t_row + q4 * 32, v32);
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (q4 * 32 + i < DVP) acc[q4 * 32 + i] = fmaf(acc[q4 * 32 + i], corr, v32[i]);
+    }
+    tc_before_sync();
+    __syncthreads();
+    tc_after_sync();
+  }
+  // epilogue
+  if (row < a.S) {
+    if (real) {
+      const float inv = 1.f / l;
+#pragma unroll
+      for (int t = 0; t < DVP; ++t)
+        if (t < a.dv) a.out[row * a.ldv + (int64_t)h * a.dv + t] = __float2bfloat16(acc[t] * inv);
+      a.lse[row * a.H + h] = m + log2f(l);
+    } else {  // pad row: attends only itself (model.cpp:400-403)
+      const float mult = a.wmult ? a.wmult[((int64_t)h * a.S + row) * a.S + row] : 1.f;
+      for (int t = 0; t < a.dv; ++t) {
+        const float vv = __bfloat162float(a.v[row * a.ldv + (int64_t)h * a.dv + t]);
+        a.out[row * a.ldv + (int64_t)h * a.dv + t] = __float2bfloat16(mult * vv);
+      }
+      a.lse[row * a.H + h] = 0.f;
+    }
+  }
+  tc_before_sync();
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
+}
+
+template <int DKP, int DVP>
+cudaError_t launch(const TcArgs& a, cudaStream_t st) {
+  const size_t smem = (size_t)kM * DKP * 2 + (size_t)kN * DKP * 2 + (size_t)DVP * kN * 2 + (size_t)kM * kN * 2 + 16;
+  cudaError_t e = cudaFuncSetAttribute(dense_tc_fwd_kernel<DKP, DVP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid((unsigned)((a.S + kM - 1) / kM), (unsigned)a.H);
+  dense_tc_fwd_kernel<DKP, DVP><<<grid, kM, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int DKP>
+cudaError_t launch_dv(const TcArgs& a, cudaStream_t st) {
+  const int dvp = (a.dv + 15) / 16 * 16;
+  switch (dvp) {
+    case 16: return launch<DKP, 16>(a, st);
+    case 32: return launch<DKP, 32>(a, st);
+    case 48: return launch<DKP, 48>(a, st);
+    default: return launch<DKP, 64>(a, st);
+  }
+}
+
+}  // namespace
+
+namespace gte_b200 {
+
+// bf16 dense forward on tcgen05 (dk, dv <= 64); the caller validated the args
+cudaError_t launch_dense_tc_fwd(int64_t S, int64_t s_real, int H, int dk, int dv, const void* q, const void* k,
+                                int64_t ldq, const void* v, int64_t ldv, const void* bias, const void* wmult,
+                                void* out, void* lse, cudaStream_t st) {
+  TcArgs a{};
+  a.S = S, a.s_real = s_real, a.H = H, a.dk = dk, a.dv = dv, a.ldq = ldq, a.ldv = ldv;
+  a.q = static_cast<const __nv_bfloat16*>(q);
+  a.k = static_cast<const __nv_bfloat16*>(k);
+  a.v = static_cast<const __nv_bfloat16*>(v);
+  a.bias = static_cast<const float*>(bias);
+  a.wmult = static_cast<const float*>(wmult);
+  a.out = static_cast<__nv_bfloat16*>(out);
+  a.lse = static_cast<float*>(lse);
+  a.scale_l = (float)(1.4426950408889634 / std::sqrt((double)dk));
+  const int dkp = (dk + 15) / 16 * 16;
+  switch (dkp) {
+    case 16: return launch_dv<16>(a, st);
+    case 32: return launch_dv<32>(a, st);
+    case 48: return launch_dv<48>(a, st);
+    default: return launch_dv<64>(a, st);
+  }
+}
+
+}  // namespace gte_b200

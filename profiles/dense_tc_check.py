@@ -1,0 +1,22 @@
+import sys, time, numpy as np, torch
+sys.path.insert(0, '.')
+from paper_2407_14106_b200 import attention as A
+for (S, s_real, H, dh) in ((300, 300, 8, 8), (300, 257, 8, 8), (1024, 1024, 8, 16), (4096, 4096, 8, 8)):
+    g = torch.Generator(device="cuda").manual_seed(0)
+    q, k, v = (torch.randn((S, H * dh), generator=g, device="cuda").to(torch.bfloat16) for _ in range(3))
+    att = A.DeviceDenseAttention(S, H, dh, dh, "bf16", s_real=s_real)
+    o, lse = att.forward(q, k, v); torch.cuda.synchronize()
+    att32 = A.DeviceDenseAttention(S, H, dh, dh, "f32", s_real=s_real)
+    o32, lse32 = att32.forward(q.float(), k.float(), v.float()); torch.cuda.synchronize()
+    e = (o.float() - o32).abs().max().item() / o32.abs().max().item()
+    el = (lse[:s_real] - lse32[:s_real]).abs().max().item()
+    # timing
+    for _ in range(3): att.forward(q, k, v)
+    torch.cuda.synchronize(); t0 = time.perf_counter()
+    for _ in range(10): att.forward(q, k, v)
+    torch.cuda.synchronize(); t = (time.perf_counter() - t0) / 10
+    for _ in range(3): att32.forward(q.float(), k.float(), v.float())
+    torch.cuda.synchronize(); t0 = time.perf_counter()
+    for _ in range(10): att32.forward(q.float(), k.float(), v.float())
+    torch.cuda.synchronize(); t32 = (time.perf_counter() - t0) / 10
+    print(f"S={S} s_real={s_real} H={H} dh={dh}: tc-vs-f32 max-norm err {e:.3e}, lse err {el:.3e}; tc fwd {t*1e3:.3f} ms, cuda-core f32 fwd {t32*1e3:.3f} ms", flush=True)
