@@ -53,6 +53,7 @@ struct TcArgs {
   __nv_bfloat16* out;
   float* lse;
   float scale_l;  // log2(e) / sqrt(dk)
+  int vec;        // 16-byte row chunks: dk, dv multiples of 8, 16-byte aligned rows
 };
 
 // byte offset of element (r, kk) in a canonical K-major no-swizzle tile whose
@@ -122,7 +123,7 @@ __device__ __forceinline__ void tc_before_sync() { asm volatile("tcgen05.fence::
 __device__ __forceinline__ void tc_after_sync() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
 template <int DKP, int DVP>
-__global__ void __launch_bounds__(kM) dense_tc_fwd_kernel(TcArgs a) {
+__global__ void __launch_bounds__(kM, 4) dense_tc_fwd_kernel(TcArgs a) {
   extern __shared__ __align__(1024) unsigned char smem[];
   unsigned char* Qs = smem;                       // [128 x DKP]
   unsigned char* Ks = Qs + kM * DKP * 2;          // [128 x DKP]
@@ -171,17 +172,36 @@ __global__ void __launch_bounds__(kM) dense_tc_fwd_kernel(TcArgs a) {
   for (int64_t c0 = 0; c0 < a.s_real; c0 += kN) {
     const int n = (int)(a.s_real - c0 < kN ? a.s_real - c0 : kN);
     // 1. stage K block and V^T block
-    for (int x = tid; x < kN * DKP; x += kM) {
-      const int c = x / DKP, kk = x % DKP;
-      __nv_bfloat16 val = __float2bfloat16(0.f);
-      if (c < n && kk < a.dk) val = a.k[(c0 + c) * a.ldq + (int64_t)h * a.dk + kk];
-      *reinterpret_cast<__nv_bfloat16*>(Ks + canon(c, kk, DKP)) = val;
-    }
-    for (int x = tid; x < kN * DVP; x += kM) {
-      const int c = x / DVP, t = x % DVP;
-      __nv_bfloat16 val = __float2bfloat16(0.f);
-      if (c < n && t < a.dv) val = a.v[(c0 + c) * a.ldv + (int64_t)h * a.dv + t];
-      *reinterpret_cast<__nv_bfloat16*>(Vt + canon(t, c, kN)) = val;
+    if (a.vec) {  // one 16-byte chunk (8 elements) per thread and step
+      for (int x = tid; x < kN * (DKP / 8); x += kM) {
+        const int c = x / (DKP / 8), kk = (x % (DKP / 8)) * 8;
+        uint4 val = make_uint4(0, 0, 0, 0);
+        if (c < n && kk < a.dk)
+          val = __ldg(reinterpret_cast<const uint4*>(a.k + (c0 + c) * a.ldq + (int64_t)h * a.dk + kk));
+        *reinterpret_cast<uint4*>(Ks + canon(c, kk, DKP)) = val;
+      }
+      for (int x = tid; x < kN * (DVP / 8); x += kM) {
+        const int c = x / (DVP / 8), t0 = (x % (DVP / 8)) * 8;
+        uint4 val = make_uint4(0, 0, 0, 0);
+        if (c < n && t0 < a.dv)
+          val = __ldg(reinterpret_cast<const uint4*>(a.v + (c0 + c) * a.ldv + (int64_t)h * a.dv + t0));
+        const __nv_bfloat16* e8 = reinterpret_cast<const __nv_bfloat16*>(&val);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) *reinterpret_cast<__nv_bfloat16*>(Vt + canon(t0 + t, c, kN)) = e8[t];
+      }
+    } else {
+      for (int x = tid; x < kN * DKP; x += kM) {
+        const int c = x / DKP, kk = x % DKP;
+        __nv_bfloat16 val = __float2bfloat16(0.f);
+        if (c < n && kk < a.dk) val = a.k[(c0 + c) * a.ldq + (int64_t)h * a.dk + kk];
+        *reinterpret_cast<__nv_bfloat16*>(Ks + canon(c, kk, DKP)) = val;
+      }
+      for (int x = tid; x < kN * DVP; x += kM) {
+        const int c = x / DVP, t = x % DVP;
+        __nv_bfloat16 val = __float2bfloat16(0.f);
+        if (c < n && t < a.dv) val = a.v[(c0 + c) * a.ldv + (int64_t)h * a.dv + t];
+        *reinterpret_cast<__nv_bfloat16*>(Vt + canon(t, c, kN)) = val;
+      }
     }
     fence_async_smem();
     tc_before_sync();
@@ -198,43 +218,51 @@ __global__ void __launch_bounds__(kM) dense_tc_fwd_kernel(TcArgs a) {
     mbar_wait(bar, phase);
     phase ^= 1;
     tc_after_sync();
-    // 3. online softmax on this thread's row
-    float s[kN];
+    // 3. online softmax on this thread's row, two passes over TMEM (max, then
+    //    p): 32 scores live at a time keeps the CTA at ~100 registers
+    float mx = -INFINITY;
 #pragma unroll
     for (int q4 = 0; q4 < kN / 32; ++q4) {
       float v32[32];
       tmem_ld32(t_row + q4 * 32, v32);
 #pragma unroll
-      for (int i = 0; i < 32; ++i) s[q4 * 32 + i] = v32[i];
-    }
-    float mx = -INFINITY;
-#pragma unroll
-    for (int c = 0; c < kN; ++c) {
-      float x = s[c] * a.scale_l;
-      if (a.bias && real && c < n) x = fmaf(a.bias[row * a.S + c0 + c], 1.4426950408889634f, x);
-      s[c] = c < n ? x : -INFINITY;
-      mx = fmaxf(mx, s[c]);
+      for (int i = 0; i < 32; ++i) {
+        const int c = q4 * 32 + i;
+        float x = v32[i] * a.scale_l;
+        if (a.bias && real && c < n) x = fmaf(a.bias[row * a.S + c0 + c], 1.4426950408889634f, x);
+        mx = fmaxf(mx, c < n ? x : -INFINITY);
+      }
     }
     const float mn = fmaxf(m, mx);
     const float corr = exp2f(m - mn);
     l *= corr;
 #pragma unroll
-    for (int c8 = 0; c8 < kN / 8; ++c8) {
-      uint32_t w[4];
+    for (int q4 = 0; q4 < kN / 32; ++q4) {
+      float v32[32];
+      tmem_ld32(t_row + q4 * 32, v32);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int c = c8 * 8 + 2 * i;
-        float p0 = exp2f(s[c] - mn), p1 = exp2f(s[c + 1] - mn);
-        l += p0 + p1;
-        if (a.wmult && real) {
-          const float* wr = a.wmult + ((int64_t)h * a.S + row) * a.S + c0;
-          p0 = c < n ? p0 * wr[c] : 0.f;
-          p1 = c + 1 < n ? p1 * wr[c + 1] : 0.f;
+      for (int c8 = 0; c8 < 4; ++c8) {
+        uint32_t w[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int j = c8 * 8 + 2 * i, c = q4 * 32 + j;
+          float x0 = v32[j] * a.scale_l, x1 = v32[j + 1] * a.scale_l;
+          if (a.bias && real) {
+            if (c < n) x0 = fmaf(a.bias[row * a.S + c0 + c], 1.4426950408889634f, x0);
+            if (c + 1 < n) x1 = fmaf(a.bias[row * a.S + c0 + c + 1], 1.4426950408889634f, x1);
+          }
+          float p0 = c < n ? exp2f(x0 - mn) : 0.f, p1 = c + 1 < n ? exp2f(x1 - mn) : 0.f;
+          l += p0 + p1;
+          if (a.wmult && real) {
+            const float* wr = a.wmult + ((int64_t)h * a.S + row) * a.S + c0;
+            p0 = c < n ? p0 * wr[c] : 0.f;
+            p1 = c + 1 < n ? p1 * wr[c + 1] : 0.f;
+          }
+          __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
+          w[i] = *reinterpret_cast<uint32_t*>(&b2);
         }
-        __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
-        w[i] = *reinterpret_cast<uint32_t*>(&b2);
+        *reinterpret_cast<uint4*>(Ps + canon(tid, q4 * 32 + c8 * 8, kN)) = make_uint4(w[0], w[1], w[2], w[3]);
       }
-      *reinterpret_cast<uint4*>(Ps + canon(tid, c8 * 8, kN)) = make_uint4(w[0], w[1], w[2], w[3]);
     }
     m = mn;
     fence_async_smem();
@@ -326,6 +354,8 @@ cudaError_t launch_dense_tc_fwd(int64_t S, int64_t s_real, int H, int dk, int dv
   a.out = static_cast<__nv_bfloat16*>(out);
   a.lse = static_cast<float*>(lse);
   a.scale_l = (float)(1.4426950408889634 / std::sqrt((double)dk));
+  a.vec = dk % 8 == 0 && dv % 8 == 0 && (ldq * 2) % 16 == 0 && (ldv * 2) % 16 == 0 &&
+          (reinterpret_cast<uintptr_t>(k) % 16) == 0 && (reinterpret_cast<uintptr_t>(v) % 16) == 0;
   const int dkp = (dk + 15) / 16 * 16;
   switch (dkp) {
     case 16: return launch_dv<16>(a, st);

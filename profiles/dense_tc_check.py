@@ -1,7 +1,11 @@
 import sys, time, numpy as np, torch
 sys.path.insert(0, '.')
 from paper_2407_14106_b200 import attention as A
-for (S, s_real, H, dh) in ((300, 300, 8, 8), (300, 257, 8, 8), (1024, 1024, 8, 16), (4096, 4096, 8, 8)):
+import os
+CASES = ((300, 300, 8, 8), (300, 257, 8, 8), (1024, 1024, 8, 16), (4096, 4096, 8, 8), (32768, 32768, 8, 8), (32768, 32768, 8, 16))
+if os.environ.get('DENSE_CASE'):
+    CASES = (CASES[int(os.environ['DENSE_CASE'])],)
+for (S, s_real, H, dh) in CASES:
     g = torch.Generator(device="cuda").manual_seed(0)
     q, k, v = (torch.randn((S, H * dh), generator=g, device="cuda").to(torch.bfloat16) for _ in range(3))
     att = A.DeviceDenseAttention(S, H, dh, dh, "bf16", s_real=s_real)
@@ -19,4 +23,8 @@ for (S, s_real, H, dh) in ((300, 300, 8, 8), (300, 257, 8, 8), (1024, 1024, 8, 1
     torch.cuda.synchronize(); t0 = time.perf_counter()
     for _ in range(10): att32.forward(q.float(), k.float(), v.float())
     torch.cuda.synchronize(); t32 = (time.perf_counter() - t0) / 10
-    print(f"S={S} s_real={s_real} H={H} dh={dh}: tc-vs-f32 max-norm err {e:.3e}, lse err {el:.3e}; tc fwd {t*1e3:.3f} ms, cuda-core f32 fwd {t32*1e3:.3f} ms", flush=True)
+    pairs = s_real * s_real * H
+    exps_bound = pairs / (148 * 16 * 1.965e9)  # MUFU ex2: 16 / clk / SM
+    print(f"S={S} s_real={s_real} H={H} dh={dh}: tc-vs-f32 max-norm err {e:.3e}, lse err {el:.3e}; tc fwd {t*1e3:.3f} ms "
+          f"({pairs / t / 1e12:.2f} T pair-heads/s, {exps_bound / t * 100:.1f}% of the MUFU exp bound, "
+          f"{4 * dh * pairs / t / 1e12:.1f} TFLOP/s algorithmic), cuda-core f32 fwd {t32*1e3:.3f} ms", flush=True)
