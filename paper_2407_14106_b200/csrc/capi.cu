@@ -114,6 +114,8 @@ unsigned grid_for(int64_t n, int block = 256) {
 struct gte_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy = nullptr;          // host<->device copies of the *_host entries (lazy)
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   int* d_err = nullptr;  // [0] non-finite bits, [1] first empty row
   int* h_err = nullptr;  // pinned mirror
   int64_t launches = 0;
@@ -659,6 +661,11 @@ int gte_ctx_destroy(gte_ctx* c) {
   if (!c) return GTE_OK;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
+  if (c->copy) {
+    cudaStreamSynchronize(c->copy);
+    cudaStreamDestroy(c->copy);
+    for (auto& e : c->ev) cudaEventDestroy(e);
+  }
   for (auto& b : c->io) b.release();
   cudaFree(c->d_err);
   cudaFreeHost(c->h_err);
@@ -979,24 +986,43 @@ int gte_sparse_attn_fwd_bwd_host(gte_ctx* c, const gte_plan* plan, int dtype, in
   CUDA_TRY(c->io[4].ensure(S * H * as));
   CUDA_TRY(c->io[5].ensure((E + 1) * as));
   CUDA_TRY(c->io[6].ensure((E + 1) * as));
-  CUDA_TRY(cudaMemcpyAsync(c->io[0].p, q, bq, cudaMemcpyHostToDevice, st));
-  CUDA_TRY(cudaMemcpyAsync(c->io[1].p, k, bq, cudaMemcpyHostToDevice, st));
-  CUDA_TRY(cudaMemcpyAsync(c->io[2].p, v, bv, cudaMemcpyHostToDevice, st));
-  CUDA_TRY(cudaMemcpyAsync(c->io[9].p, dout, bv, cudaMemcpyHostToDevice, st));
-  if (bias) CUDA_TRY(cudaMemcpyAsync(c->io[6].p, bias, E * as, cudaMemcpyHostToDevice, st));
+  // copies on a second stream, ordered against the kernels with events: dO
+  // travels while the forward runs, O comes back while the backward runs
+  if (!c->copy) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+    for (auto& e : c->ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  cudaStream_t cp = c->copy;
+  CUDA_TRY(cudaEventRecord(c->ev[3], st));  // earlier work on the compute stream (buffers free)
+  CUDA_TRY(cudaStreamWaitEvent(cp, c->ev[3], 0));
+  CUDA_TRY(cudaMemcpyAsync(c->io[1].p, k, bq, cudaMemcpyHostToDevice, cp));
+  CUDA_TRY(cudaMemcpyAsync(c->io[2].p, v, bv, cudaMemcpyHostToDevice, cp));
+  CUDA_TRY(cudaMemcpyAsync(c->io[0].p, q, bq, cudaMemcpyHostToDevice, cp));
+  if (bias) CUDA_TRY(cudaMemcpyAsync(c->io[6].p, bias, E * as, cudaMemcpyHostToDevice, cp));
+  CUDA_TRY(cudaEventRecord(c->ev[0], cp));  // forward inputs resident
+  CUDA_TRY(cudaMemcpyAsync(c->io[9].p, dout, bv, cudaMemcpyHostToDevice, cp));
+  CUDA_TRY(cudaEventRecord(c->ev[1], cp));  // dO resident
   const void* bias_dev = bias ? c->io[6].p : nullptr;
+  CUDA_TRY(cudaStreamWaitEvent(st, c->ev[0], 0));
   rc = gte_sparse_attn_fwd(c, plan, dtype, H, dk, dv, c->io[0].p, c->io[1].p, (int64_t)H * dk, c->io[2].p,
                            (int64_t)H * dv, bias_dev, nullptr, c->io[3].p, c->io[4].p, 0);
   if (rc) return rc;
+  CUDA_TRY(cudaEventRecord(c->ev[2], st));  // O ready
+  CUDA_TRY(cudaStreamWaitEvent(cp, c->ev[2], 0));
+  CUDA_TRY(cudaMemcpyAsync(out, c->io[3].p, bv, cudaMemcpyDeviceToHost, cp));
+  CUDA_TRY(cudaStreamWaitEvent(st, c->ev[1], 0));
   rc = gte_sparse_attn_bwd(c, plan, dtype, H, dk, dv, c->io[0].p, c->io[1].p, (int64_t)H * dk, c->io[2].p,
                            (int64_t)H * dv, c->io[3].p, c->io[4].p, c->io[9].p, bias_dev, nullptr,
                            c->io[7].p, c->io[8].p, c->io[10].p, c->io[5].p);
   if (rc) return rc;
-  CUDA_TRY(cudaMemcpyAsync(out, c->io[3].p, bv, cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaMemcpyAsync(dq, c->io[7].p, bq, cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaMemcpyAsync(dk_out, c->io[8].p, bq, cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaMemcpyAsync(dv_out, c->io[10].p, bv, cudaMemcpyDeviceToHost, st));
-  if (dbias && E) CUDA_TRY(cudaMemcpyAsync(dbias, c->io[5].p, E * as, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaEventRecord(c->ev[3], st));  // gradients ready
+  CUDA_TRY(cudaStreamWaitEvent(cp, c->ev[3], 0));
+  CUDA_TRY(cudaMemcpyAsync(dq, c->io[7].p, bq, cudaMemcpyDeviceToHost, cp));
+  CUDA_TRY(cudaMemcpyAsync(dk_out, c->io[8].p, bq, cudaMemcpyDeviceToHost, cp));
+  CUDA_TRY(cudaMemcpyAsync(dv_out, c->io[10].p, bv, cudaMemcpyDeviceToHost, cp));
+  if (dbias && E) CUDA_TRY(cudaMemcpyAsync(dbias, c->io[5].p, E * as, cudaMemcpyDeviceToHost, cp));
+  CUDA_TRY(cudaEventRecord(c->ev[0], cp));
+  CUDA_TRY(cudaStreamWaitEvent(st, c->ev[0], 0));  // drain_errors below synchronises st
   return drain_errors(c);
 }
 

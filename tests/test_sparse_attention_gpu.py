@@ -319,3 +319,26 @@ def test_padded_kernels_match_tile_kernels(cuda, dtype, variant):
         e_max, e_nrm = rel_err(x, y)
         tol = 1e-5 if dtype == "f32" else 1e-2
         assert e_max <= tol and e_nrm <= tol, f"{nm}: {e_max:.3g} {e_nrm:.3g}"
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_fwd_bwd_host_matches_device_path(cuda, dtype):
+    """gte_sparse_attn_fwd_bwd_host (pinned host buffers, copies on a second
+    stream overlapped with the kernels) == the device-resident path, bit for
+    bit, over repeated calls (the bench's e2e leg)."""
+    import torch
+
+    ro, co = community_graph(6000, 10.0, community=64, seed=8)
+    r = run_device(ro, co, 8, 8, dtype, seed=9)
+    td = _torch_dtype(dtype)
+    pin = lambda a, t: torch.tensor(a, dtype=t).pin_memory()  # noqa: E731
+    hq, hk, hv, hdo = (pin(r[n], td) for n in ("q", "k", "v", "do"))
+    hb = pin(r["bias"], torch.float32)
+    plan = A.DevicePlan.from_host(ro, co)
+    att = A.DeviceSparseAttention(plan, 8, 8, 8, dtype)
+    outs = [torch.empty(hv.shape, dtype=td).pin_memory() for _ in range(4)]
+    hdb = torch.empty(co.shape[0], dtype=torch.float32).pin_memory()
+    for _ in range(3):
+        att.fwd_bwd_host(hq, hk, hv, hdo, hb, *outs, hdb)
+    for got, nm in zip(outs + [hdb], ("out", "dq", "dk", "dv", "db")):
+        assert np.array_equal(got.double().numpy(), r[nm]), nm
