@@ -118,6 +118,12 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void tc_before_sync() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_after_sync() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -219,22 +225,33 @@ __global__ void __launch_bounds__(kM, 4) dense_tc_fwd_kernel(TcArgs a) {
     phase ^= 1;
     tc_after_sync();
     // 3. online softmax on this thread's row, two passes over TMEM (max, then
-    //    p): 32 scores live at a time keeps the CTA at ~100 registers
+    //    p): 32 scores live at a time keeps the CTA at ~100 registers. Without
+    //    a bias the scale folds into one FFMA per score: max(scale*s) =
+    //    scale*max(s) (scale > 0), p = ex2(s*scale - m).
     float mx = -INFINITY;
 #pragma unroll
     for (int q4 = 0; q4 < kN / 32; ++q4) {
       float v32[32];
       tmem_ld32(t_row + q4 * 32, v32);
+      if (a.bias) {
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const int c = q4 * 32 + i;
-        float x = v32[i] * a.scale_l;
-        if (a.bias && real && c < n) x = fmaf(a.bias[row * a.S + c0 + c], 1.4426950408889634f, x);
-        mx = fmaxf(mx, c < n ? x : -INFINITY);
+        for (int i = 0; i < 32; ++i) {
+          const int c = q4 * 32 + i;
+          float x = v32[i] * a.scale_l;
+          if (real && c < n) x = fmaf(a.bias[row * a.S + c0 + c], 1.4426950408889634f, x);
+          mx = fmaxf(mx, c < n ? x : -INFINITY);
+        }
+      } else if (q4 * 32 + 32 <= n) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) mx = fmaxf(mx, v32[i]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) mx = fmaxf(mx, q4 * 32 + i < n ? v32[i] : -INFINITY);
       }
     }
+    if (!a.bias) mx *= a.scale_l;
     const float mn = fmaxf(m, mx);
-    const float corr = exp2f(m - mn);
+    const float corr = ex2_approx(m - mn);
     l *= corr;
 #pragma unroll
     for (int q4 = 0; q4 < kN / 32; ++q4) {
@@ -246,12 +263,12 @@ __global__ void __launch_bounds__(kM, 4) dense_tc_fwd_kernel(TcArgs a) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int j = c8 * 8 + 2 * i, c = q4 * 32 + j;
-          float x0 = v32[j] * a.scale_l, x1 = v32[j + 1] * a.scale_l;
+          float x0 = fmaf(v32[j], a.scale_l, -mn), x1 = fmaf(v32[j + 1], a.scale_l, -mn);
           if (a.bias && real) {
             if (c < n) x0 = fmaf(a.bias[row * a.S + c0 + c], 1.4426950408889634f, x0);
             if (c + 1 < n) x1 = fmaf(a.bias[row * a.S + c0 + c + 1], 1.4426950408889634f, x1);
           }
-          float p0 = c < n ? exp2f(x0 - mn) : 0.f, p1 = c + 1 < n ? exp2f(x1 - mn) : 0.f;
+          float p0 = c < n ? ex2_approx(x0) : 0.f, p1 = c + 1 < n ? ex2_approx(x1) : 0.f;
           l += p0 + p1;
           if (a.wmult && real) {
             const float* wr = a.wmult + ((int64_t)h * a.S + row) * a.S + c0;
