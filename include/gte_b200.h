@@ -224,6 +224,27 @@ int gte_dense_attn_bwd_host(gte_ctx* ctx, int dtype, int64_t S, int64_t s_real, 
                             const void* k, const void* v, const void* bias, const void* wmult, const void* dout,
                             void* dq, void* dk_out, void* dv_out, void* dbias);
 
+/* ---- Trainer glue (reference model.cpp:76-83, 407-423, 447-463, 520-523) ----
+ * extend_with_pad_loops: rows [rows, s_pad) get one self-loop each (host;
+ * out_row_off [max(rows, s_pad) + 1], out_cols [nnz + max(0, s_pad - rows)]).
+ * pattern_buckets: SPD bias bucket per attended pair, the Trainer's rule: 0
+ * for the same token, 1 if either is the global token, max_dist + 1 if either
+ * lies past the SPD table (pads) or the pair is absent from it, else its
+ * distance (SpdTable::lookup, graph.cpp:208-214). The SPD table is the
+ * reference's sparse CSR (row_off int64 [spd_n + 1], cols int64, dist uint16).
+ * bias_from_table: bias[e] = table[bucket[e]]; dbias_to_table: the table's
+ * gradient, summed in a fixed order (workspace: 296 * n_buckets floats). */
+int gte_extend_with_pad_loops_host(int64_t rows, int64_t nnz, const int64_t* row_off, const int64_t* cols,
+                                   int64_t s_pad, int64_t* out_row_off, int64_t* out_cols);
+int gte_pattern_buckets(gte_ctx* ctx, int64_t rows, int64_t nnz, const int32_t* d_row_ptr, const int32_t* d_cols,
+                        const int64_t* d_perm_inverse, int64_t global_index, int64_t spd_n,
+                        const int64_t* d_spd_row_off, const int64_t* d_spd_cols, const uint16_t* d_spd_dist,
+                        int64_t max_dist, int32_t* d_buckets);
+int gte_bias_from_table(gte_ctx* ctx, int64_t nnz, const int32_t* d_buckets, const float* d_table, int64_t n_buckets,
+                        float* d_bias);
+int gte_dbias_to_table(gte_ctx* ctx, int64_t nnz, const int32_t* d_buckets, const float* d_dbias, int64_t n_buckets,
+                       float* d_table_grad, float* d_workspace);
+
 /* ---- sequence parallelism (reference parallel.cpp:115-332, Ulysses
  * head-split all-to-all) ----
  * gte_sp: the exchange plan of P workers — token ids per worker (worker-major,

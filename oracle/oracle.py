@@ -262,6 +262,23 @@ class Oracle(_Base):
         self._call("select_db", C.c_int64(db.shape[0]), _ptr(db, I64P), _ptr(thr), C.byref(out))
         return out.value
 
+    def pattern_buckets(self, pat: CSR, perm_inv, global_index, spd, max_dist):
+        """model.cpp:447-463 bucket fill; spd = (row_off, cols, dist uint16, n)."""
+        ro, co, dist, n = spd
+        out = np.zeros(max(pat.nnz, 1), dtype=np.int32)
+        pc = pat.to_c()
+        d16 = np.ascontiguousarray(dist, dtype=np.uint16)
+        self._call("pattern_buckets", C.byref(pc), _ptr(_i64(perm_inv), I64P), C.c_int64(global_index),
+                   C.c_int64(n), _ptr(_i64(ro), I64P), _ptr(_i64(co), I64P),
+                   d16.ctypes.data_as(C.POINTER(C.c_uint16)), C.c_int64(max_dist), _ptr(out, I32P))
+        return out[: pat.nnz]
+
+    def extend_with_pad_loops(self, pat: CSR, s_pad) -> CSR:
+        out = _CCsr()
+        pc = pat.to_c()
+        self._call("extend_with_pad_loops", C.byref(pc), C.c_int64(s_pad), C.byref(out))
+        return self._take_csr(out)
+
     def check_conditions(self, g: CSR, layers):
         r = _OrcCond()
         gc = g.to_c()
@@ -477,6 +494,19 @@ class RefOracle(_Base):
         self._call("check_conditions", C.byref(gc), C.c_int64(layers), _ptr(flags, I32P), _ptr(ints, I64P))
         return dict(c1=bool(flags[0]), c2=bool(flags[1]), c3=bool(flags[2]), layers=int(ints[0]),
                     sweep_from=int(ints[1]), sweep_to=int(ints[2]), diameter_lower_bound=int(ints[3]))
+
+    def spd_table(self, g: CSR, max_dist):
+        """The compiled reference's gte::spd_table (graph.cpp:216-262)."""
+        ro, co, di = C.POINTER(C.c_int64)(), C.POINTER(C.c_int64)(), C.POINTER(C.c_uint16)()
+        nnz = C.c_int64()
+        gc = g.to_c()
+        self._call("spd_table", C.byref(gc), C.c_int64(max_dist), C.byref(ro), C.byref(co), C.byref(di), C.byref(nnz))
+        n, m = g.n, nnz.value
+        out = (np.ctypeslib.as_array(ro, (n + 1,)).copy(), np.ctypeslib.as_array(co, (max(m, 1),))[:m].copy(),
+               np.ctypeslib.as_array(di, (max(m, 1),))[:m].copy(), n)
+        for p_ in (ro, co, di):
+            self.lib.refc_free(C.cast(p_, C.c_void_p))
+        return out
 
     def generate_sbm(self, n, blocks, pin, pout, seed, noise=0.0):
         out = _CCsr()

@@ -144,3 +144,52 @@ int orc_dist_layer_bwd(int64_t P, int64_t S_pad, int64_t d, int64_t H, const int
   free(qh); free(kh); free(vh); free(uh); free(gq); free(gk); free(gv); free(gb);
   return rc;
 }
+
+/* ---- Trainer glue ---- */
+
+/* proj/src/model.cpp:76-83 */
+int orc_extend_with_pad_loops(const orc_csr* pat, int64_t s_pad, orc_csr* out) {
+  const int64_t n = pat->n, extra = s_pad > n ? s_pad - n : 0;
+  out->n = n + extra;
+  out->nnz = pat->nnz + extra;
+  out->row_off = (int64_t*)malloc(sizeof(int64_t) * (size_t)(out->n + 1));
+  out->cols = (int64_t*)malloc(sizeof(int64_t) * (size_t)(out->nnz > 0 ? out->nnz : 1));
+  for (int64_t r = 0; r <= n; ++r) out->row_off[r] = pat->row_off[r];
+  for (int64_t e = 0; e < pat->nnz; ++e) out->cols[e] = pat->cols[e];
+  for (int64_t r = n; r < n + extra; ++r) {
+    out->cols[out->row_off[r]] = r;
+    out->row_off[r + 1] = out->row_off[r] + 1;
+  }
+  return ORC_OK;
+}
+
+/* SpdTable::lookup, proj/src/graph.cpp:208-214 (lower_bound in row i) */
+static int64_t spd_lookup(const int64_t* ro, const int64_t* cols, const uint16_t* dist, int64_t i, int64_t j,
+                          int64_t unreachable) {
+  int64_t lo = ro[i], hi = ro[i + 1];
+  while (lo < hi) {
+    const int64_t mid = lo + (hi - lo) / 2;
+    if (cols[mid] < j) lo = mid + 1; else hi = mid;
+  }
+  if (lo < ro[i + 1] && cols[lo] == j) return dist[lo];
+  return unreachable;
+}
+
+/* proj/src/model.cpp:447-463 (layout_for) / :407-423 (bucket_of) */
+int orc_pattern_buckets(const orc_csr* pat, const int64_t* perm_inv, int64_t global_index, int64_t spd_n,
+                        const int64_t* spd_row_off, const int64_t* spd_cols, const uint16_t* spd_dist,
+                        int64_t max_dist, int32_t* buckets) {
+  int64_t p = 0;
+  for (int64_t r = 0; r < pat->n; ++r) {
+    for (int64_t e = pat->row_off[r]; e < pat->row_off[r + 1]; ++e) {
+      const int64_t i = perm_inv[r], j = perm_inv[pat->cols[e]];
+      int64_t b;
+      if (i == j) b = 0;
+      else if (i == global_index || j == global_index) b = 1;
+      else if (i >= spd_n || j >= spd_n) b = max_dist + 1;
+      else b = spd_lookup(spd_row_off, spd_cols, spd_dist, i, j, max_dist + 1);
+      buckets[p++] = (int32_t)b;
+    }
+  }
+  return ORC_OK;
+}

@@ -420,4 +420,21 @@ int refc_select_db(int64_t n, const int64_t* db, const double* thr, int64_t* out
   });
 }
 
+
+// gte::spd_table (proj/src/graph.cpp:216-262): malloc-owned CSR + distances
+int refc_spd_table(const CCsr* g, int64_t max_dist, int64_t** row_off, int64_t** cols, uint16_t** dist,
+                   int64_t* nnz) {
+  return guard([&] {
+    Graph gr = from_c(g);
+    SpdTable t = spd_table(gr, static_cast<int>(max_dist));
+    *nnz = static_cast<int64_t>(t.cols.size());
+    *row_off = static_cast<int64_t*>(std::malloc(sizeof(int64_t) * t.row_offsets.size()));
+    *cols = static_cast<int64_t*>(std::malloc(sizeof(int64_t) * (t.cols.size() + 1)));
+    *dist = static_cast<uint16_t*>(std::malloc(sizeof(uint16_t) * (t.dist.size() + 1)));
+    std::memcpy(*row_off, t.row_offsets.data(), sizeof(int64_t) * t.row_offsets.size());
+    std::memcpy(*cols, t.cols.data(), sizeof(int64_t) * t.cols.size());
+    std::memcpy(*dist, t.dist.data(), sizeof(uint16_t) * t.dist.size());
+  });
+}
+
 }  // extern "C"

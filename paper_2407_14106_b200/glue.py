@@ -1,0 +1,86 @@
+"""Trainer glue around the attention kernels (reference
+proj/src/model.cpp:76-83, 407-423, 447-463, 520-523): pad loops on the
+pattern, SPD bias buckets per attended pair, the per-pair bias gathered from
+the layer's bucket table and the table's gradient. All computation in
+libgte_b200.so (csrc/glue.cu); torch tensors are device-memory plumbing."""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from ._lib import check
+from .attention import Context
+
+VP, I64 = C.c_void_p, C.c_int64
+
+
+def _bind():
+    L = _lib.lib()
+    if not getattr(L, "_glue_bound", False):
+        L.gte_extend_with_pad_loops_host.argtypes = [I64, I64, VP, VP, I64, VP, VP]
+        L.gte_pattern_buckets.argtypes = [VP, I64, I64, VP, VP, VP, I64, I64, VP, VP, VP, I64, VP]
+        L.gte_bias_from_table.argtypes = [VP, I64, VP, VP, I64, VP]
+        L.gte_dbias_to_table.argtypes = [VP, I64, VP, VP, I64, VP, VP]
+        L._glue_bound = True
+    return L
+
+
+def extend_with_pad_loops(row_offsets, cols, s_pad: int):
+    """model.cpp:76-83 -> (row_offsets, cols) with one self-loop per pad row."""
+    ro = np.ascontiguousarray(row_offsets, dtype=np.int64)
+    co = np.ascontiguousarray(cols, dtype=np.int64)
+    rows = ro.shape[0] - 1
+    extra = max(0, s_pad - rows)
+    oro = np.zeros(rows + extra + 1, dtype=np.int64)
+    oco = np.zeros(max(co.shape[0] + extra, 1), dtype=np.int64)
+    check(_bind().gte_extend_with_pad_loops_host(rows, co.shape[0], ro.ctypes.data,
+                                                 co.ctypes.data if co.shape[0] else None, s_pad, oro.ctypes.data,
+                                                 oco.ctypes.data))
+    return oro, oco[: co.shape[0] + extra]
+
+
+def pattern_buckets(row_offsets, cols, perm_inverse, global_index: int, spd, max_dist: int, ctx: Context | None = None):
+    """Bucket per attended pair (model.cpp:447-463). spd = (row_off, cols, dist
+    uint16, num_nodes) — the reference SpdTable. Returns an int32 CUDA tensor."""
+    import torch
+
+    ctx = ctx or Context.get(0)
+    dev = torch.device("cuda", ctx.device)
+    ro = torch.tensor(np.asarray(row_offsets, dtype=np.int32), device=dev)
+    co = torch.tensor(np.asarray(cols, dtype=np.int32), device=dev)
+    inv = torch.tensor(np.asarray(perm_inverse, dtype=np.int64), device=dev)
+    sro, sco, sdi, sn = spd
+    t_sro = torch.tensor(np.asarray(sro, dtype=np.int64), device=dev)
+    t_sco = torch.tensor(np.asarray(sco, dtype=np.int64) if len(sco) else np.zeros(1, np.int64), device=dev)
+    t_sdi = torch.tensor(np.asarray(sdi, dtype=np.int16).view(np.int16) if len(sdi) else np.zeros(1, np.int16),
+                         device=dev)
+    out = torch.empty(max(co.numel(), 1), dtype=torch.int32, device=dev)
+    check(_bind().gte_pattern_buckets(ctx.h, ro.numel() - 1, co.numel(), ro.data_ptr(), co.data_ptr(),
+                                      inv.data_ptr(), global_index, sn, t_sro.data_ptr(), t_sco.data_ptr(),
+                                      t_sdi.data_ptr(), max_dist, out.data_ptr()))
+    return out[: co.numel()]
+
+
+def bias_from_table(buckets, table, ctx: Context | None = None):
+    """bias[e] = spd_bias[bucket[e]] (model.cpp:520-523); CUDA tensors."""
+    import torch
+
+    ctx = ctx or Context.get(0)
+    bias = torch.empty(buckets.numel(), dtype=torch.float32, device=buckets.device)
+    check(_bind().gte_bias_from_table(ctx.h, buckets.numel(), buckets.data_ptr(), table.data_ptr(), table.numel(),
+                                      bias.data_ptr()))
+    return bias
+
+
+def dbias_to_table(buckets, dbias, n_buckets: int, ctx: Context | None = None):
+    """Gradient of the bucket table: sum of dbias per bucket (fixed order)."""
+    import torch
+
+    ctx = ctx or Context.get(0)
+    out = torch.empty(n_buckets, dtype=torch.float32, device=buckets.device)
+    ws = torch.empty(296 * n_buckets, dtype=torch.float32, device=buckets.device)
+    check(_bind().gte_dbias_to_table(ctx.h, buckets.numel(), buckets.data_ptr(), dbias.data_ptr(), n_buckets,
+                                     out.data_ptr(), ws.data_ptr()))
+    return out
