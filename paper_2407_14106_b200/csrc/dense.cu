@@ -36,6 +36,10 @@ namespace gte_b200 {
 cudaError_t launch_dense_tc_fwd(int64_t S, int64_t s_real, int H, int dk, int dv, const void* q, const void* k,
                                 int64_t ldq, const void* v, int64_t ldv, const void* bias, const void* wmult,
                                 void* out, void* lse, cudaStream_t st);
+cudaError_t launch_dense_tc_bwd(int64_t S, int64_t s_real, int H, int dk, int dv, const void* q, const void* k,
+                                int64_t ldq, const void* v, int64_t ldv, const void* out, const void* lse,
+                                const void* dout, const void* bias, void* dq, void* dk_out, void* dv_out,
+                                cudaStream_t st);
 int set_error(int code, const std::string& msg);
 int64_t& ctx_launch_counter(gte_ctx* c);
 void* ctx_stream(gte_ctx* c);
@@ -464,6 +468,15 @@ int gte_dense_attn_bwd(gte_ctx* ctx, int dtype, int64_t S, int64_t s_real, int H
   a.dq = dq, a.dk_out = dk_out, a.dv_out = dv_out, a.dbias = dbias;
   a.scale = 1.0 / std::sqrt((double)dk);
   cudaStream_t st = (cudaStream_t)ctx_stream(ctx);
+  static const bool tc = [] {  // bf16 without weight_mult / dbias: tcgen05 (dense_tc.cu)
+    const char* e = getenv("GTE_DENSE_TC");
+    return !(e && e[0] == '0');
+  }();
+  if (dtype == GTE_BF16 && tc && !wmult && !dbias) {
+    DCUDA(launch_dense_tc_bwd(S, s_real, H, dk, dv, q, k, ldq, v, ldv, out, lse, dout, bias, dq, dk_out, dv_out, st));
+    ctx_launch_counter(ctx) += 2;
+    return GTE_OK;
+  }
   if (dbias) DCUDA(cudaMemsetAsync(dbias, 0, sizeof(double) / (dtype == GTE_F64 ? 1 : 2) * (size_t)S * S, st));
   DCUDA(launch(dtype, 1, a, st));
   DCUDA(launch(dtype, 2, a, st));

@@ -353,6 +353,392 @@ cudaError_t launch_dv(const TcArgs& a, cudaStream_t st) {
   }
 }
 
+
+// ===========================================================================
+// Backward on tcgen05 (bf16, no weight_mult, no dbias — those take the CUDA-
+// core kernels of dense.cu). FA2-style, atomic-free, two kernels:
+//   dq:    per 128 query rows: S = Q K^T, p = ex2(S*scale - lse); dP = dO V^T;
+//          dS = p (dP - delta) -> smem (bf16); dQ += dS K (TMEM accumulator)
+//   dkdv:  per 128 keys: S^T = K Q^T, p^T; dP^T = V dO^T; dV += P^T dO,
+//          dK += dS^T Q (two TMEM accumulators)
+// B operands that the second GEMM needs with the key / query index as K are
+// staged a second time in the canonical MN-major layout (8 k-rows x 16 B of
+// n per core matrix; LBO = 128 B along k, SBO = 2048 B along n).
+
+// MN-major canonical offset: k index (keys / queries, 128 of them), n index
+__device__ __forceinline__ uint32_t canon_mn(int kidx, int n) {
+  return (uint32_t)((n >> 3) * 2048 + (kidx >> 3) * 128 + (kidx & 7) * 16 + (n & 7) * 2);
+}
+
+__host__ __device__ constexpr uint32_t instr_desc_bmn(int M, int N) { return instr_desc(M, N) | (1u << 16); }
+
+struct TcBwdArgs {
+  int64_t S, s_real;
+  int H, dk, dv;
+  int64_t ldq, ldv;
+  const __nv_bfloat16 *q, *k, *v, *o, *dout;
+  const float* bias;  // [S*S] or null (score input only)
+  const float* lse;   // [S*H] log2 units (forward)
+  __nv_bfloat16 *dq, *dk_out, *dv_out;
+  float scale_l, scale;
+};
+
+__device__ __forceinline__ __nv_bfloat16 bz() { return __float2bfloat16(0.f); }
+
+// stage rows [r0, r0+n) of a [S x (H*W)] bf16 tensor, head h, W valid of WP
+// columns, as a K-major [128 x WP] tile and (optionally) an MN-major
+// [WP x 128] tile (row index = k)
+template <int WP>
+__device__ __forceinline__ void stage_rows(const __nv_bfloat16* g, int64_t ld, int h, int W, int64_t r0, int n,
+                                           unsigned char* kmaj, unsigned char* mnmaj) {
+  for (int x = threadIdx.x; x < 128 * WP; x += 128) {
+    const int r = x / WP, c = x % WP;
+    const __nv_bfloat16 val = (r < n && c < W) ? g[(r0 + r) * ld + (int64_t)h * W + c] : bz();
+    if (kmaj) *reinterpret_cast<__nv_bfloat16*>(kmaj + canon(r, c, WP)) = val;
+    if (mnmaj) *reinterpret_cast<__nv_bfloat16*>(mnmaj + canon_mn(r, c)) = val;
+  }
+}
+
+template <int DKP, int DVP>
+__global__ void __launch_bounds__(kM, 2) dense_tc_dq_kernel(TcBwdArgs a) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  unsigned char* Qs = smem;                    // [128 x DKP] K-major (A of S)
+  unsigned char* Ds = Qs + kM * DKP * 2;       // [128 x DVP] K-major (A of dP)
+  unsigned char* Ks = Ds + kM * DVP * 2;       // [128 keys x DKP] K-major (B of S)
+  unsigned char* Vs = Ks + kN * DKP * 2;       // [128 keys x DVP] K-major (B of dP)
+  unsigned char* Km = Vs + kN * DVP * 2;       // [DKP x 128 keys] MN-major (B of dQ)
+  unsigned char* dS = Km + DKP * kN * 2;       // [128 x 128] K-major (A of dQ)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(dS + kM * kN * 2);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
+  const int tid = threadIdx.x, warp = tid >> 5, h = blockIdx.y;
+  const int64_t r0 = (int64_t)blockIdx.x * kM, row = r0 + tid;
+  const bool real = row < a.s_real;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+        (uint32_t)__cvta_generic_to_shared(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  const int nq = (int)(a.s_real - r0 < kM ? (a.s_real - r0 > 0 ? a.s_real - r0 : 0) : kM);
+  stage_rows<DKP>(a.q, a.ldq, h, a.dk, r0, nq, Qs, nullptr);
+  stage_rows<DVP>(a.dout, a.ldv, h, a.dv, r0, nq, Ds, nullptr);
+  float lse = 0.f, delta = 0.f;
+  if (real) {
+    lse = a.lse[row * a.H + h];
+    for (int t = 0; t < a.dv; ++t)
+      delta += __bfloat162float(a.dout[row * a.ldv + (int64_t)h * a.dv + t]) *
+               __bfloat162float(a.o[row * a.ldv + (int64_t)h * a.dv + t]);
+  }
+  tc_before_sync();
+  __syncthreads();
+  tc_after_sync();
+  const uint32_t tmem = *tmem_slot, t_row = tmem + ((uint32_t)(warp * 32) << 16);
+  const uint32_t sQ = (uint32_t)__cvta_generic_to_shared(Qs), sD = (uint32_t)__cvta_generic_to_shared(Ds);
+  const uint32_t sK = (uint32_t)__cvta_generic_to_shared(Ks), sV = (uint32_t)__cvta_generic_to_shared(Vs);
+  const uint32_t sKm = (uint32_t)__cvta_generic_to_shared(Km), sS = (uint32_t)__cvta_generic_to_shared(dS);
+  uint32_t phase = 0;
+  for (int64_t c0 = 0; c0 < a.s_real; c0 += kN) {
+    const int n = (int)(a.s_real - c0 < kN ? a.s_real - c0 : kN);
+    stage_rows<DKP>(a.k, a.ldq, h, a.dk, c0, n, Ks, Km);
+    stage_rows<DVP>(a.v, a.ldv, h, a.dv, c0, n, Vs, nullptr);
+    fence_async_smem();
+    tc_before_sync();
+    __syncthreads();
+    tc_after_sync();
+    if (tid == 0) {  // S = Q K^T
+#pragma unroll
+      for (int kc = 0; kc < DKP / 16; ++kc)
+        mma_bf16(tmem, smem_desc(sQ + kc * 256, 128, DKP * 16), smem_desc(sK + kc * 256, 128, DKP * 16),
+                 instr_desc(kM, kN), kc > 0);
+      mma_commit(bar);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    tc_after_sync();
+    float p[kN];
+#pragma unroll
+    for (int q4 = 0; q4 < kN / 32; ++q4) {
+      float v32[32];
+      tmem_ld32(t_row + q4 * 32, v32);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int c = q4 * 32 + i;
+        float x = fmaf(v32[i], a.scale_l, -lse);
+        if (a.bias && real && c < n) x = fmaf(a.bias[row * a.S + c0 + c], 1.4426950408889634f, x);
+        p[c] = (real && c < n) ? ex2_approx(x) : 0.f;
+      }
+    }
+    tc_before_sync();
+    __syncthreads();
+    tc_after_sync();
+    if (tid == 0) {  // dP = dO V^T (same TMEM columns; S is in registers)
+#pragma unroll
+      for (int kc = 0; kc < DVP / 16; ++kc)
+        mma_bf16(tmem, smem_desc(sD + kc * 256, 128, DVP * 16), smem_desc(sV + kc * 256, 128, DVP * 16),
+                 instr_desc(kM, kN), kc > 0);
+      mma_commit(bar);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    tc_after_sync();
+#pragma unroll
+    for (int q4 = 0; q4 < kN / 32; ++q4) {
+      float v32[32];
+      tmem_ld32(t_row + q4 * 32, v32);
+#pragma unroll
+      for (int c8 = 0; c8 < 4; ++c8) {
+        uint32_t w[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int j = c8 * 8 + 2 * i, c = q4 * 32 + j;
+          const float d0 = p[c] * (v32[j] - delta), d1 = p[c + 1] * (v32[j + 1] - delta);
+          __nv_bfloat162 b2 = __floats2bfloat162_rn(d0, d1);
+          w[i] = *reinterpret_cast<uint32_t*>(&b2);
+        }
+        *reinterpret_cast<uint4*>(dS + canon(tid, q4 * 32 + c8 * 8, kN)) = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+    }
+    fence_async_smem();
+    tc_before_sync();
+    __syncthreads();
+    tc_after_sync();
+    if (tid == 0) {  // dQ += dS K  (A = dS K-major, B = K MN-major, N = DKP)
+#pragma unroll
+      for (int kc = 0; kc < kN / 16; ++kc)
+        mma_bf16(tmem + 128, smem_desc(sS + kc * 256, 128, kN * 16), smem_desc(sKm + kc * 256, 128, 2048),
+                 instr_desc_bmn(kM, DKP), (c0 > 0 || kc > 0) ? 1u : 0u);
+      mma_commit(bar);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    tc_after_sync();
+  }
+  if (row < a.S) {
+    float g[DKP];
+    if (a.s_real > 0) {
+#pragma unroll
+      for (int q4 = 0; q4 < (DKP + 31) / 32; ++q4) {
+        float v32[32];
+        tmem_ld32(t_row + 128 + q4 * 32, v32);
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (q4 * 32 + i < DKP) g[q4 * 32 + i] = v32[i];
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < DKP; ++t)
+      if (t < a.dk) a.dq[row * a.ldq + (int64_t)h * a.dk + t] = __float2bfloat16(real ? g[t] * a.scale : 0.f);
+  }
+  tc_before_sync();
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+}
+
+template <int DKP, int DVP>
+__global__ void __launch_bounds__(kM, 2) dense_tc_dkdv_kernel(TcBwdArgs a) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  unsigned char* Ks = smem;                    // [128 keys x DKP] K-major (A of S^T)
+  unsigned char* Vs = Ks + kM * DKP * 2;       // [128 keys x DVP] K-major (A of dP^T)
+  unsigned char* Qk = Vs + kM * DVP * 2;       // [128 q x DKP] K-major (B of S^T)
+  unsigned char* Dk = Qk + kN * DKP * 2;       // [128 q x DVP] K-major (B of dP^T)
+  unsigned char* Qm = Dk + kN * DVP * 2;       // [DKP x 128 q] MN-major (B of dK)
+  unsigned char* Dm = Qm + DKP * kN * 2;       // [DVP x 128 q] MN-major (B of dV)
+  unsigned char* Pt = Dm + DVP * kN * 2;       // [128 keys x 128 q] K-major (A of dV)
+  unsigned char* St = Pt + kM * kN * 2;        // [128 keys x 128 q] K-major (A of dK)
+  float* ls = reinterpret_cast<float*>(St + kM * kN * 2);  // [128] lse of the query block
+  float* dl = ls + kN;                                     // [128] delta of the query block
+  uint64_t* bar = reinterpret_cast<uint64_t*>(dl + kN);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
+  const int tid = threadIdx.x, warp = tid >> 5, h = blockIdx.y;
+  const int64_t k0 = (int64_t)blockIdx.x * kM, key = k0 + tid;
+  const bool real = key < a.s_real;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+        (uint32_t)__cvta_generic_to_shared(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  const int nk = (int)(a.s_real - k0 < kM ? (a.s_real - k0 > 0 ? a.s_real - k0 : 0) : kM);
+  stage_rows<DKP>(a.k, a.ldq, h, a.dk, k0, nk, Ks, nullptr);
+  stage_rows<DVP>(a.v, a.ldv, h, a.dv, k0, nk, Vs, nullptr);
+  tc_before_sync();
+  __syncthreads();
+  tc_after_sync();
+  const uint32_t tmem = *tmem_slot, t_row = tmem + ((uint32_t)(warp * 32) << 16);
+  const uint32_t sK = (uint32_t)__cvta_generic_to_shared(Ks), sV = (uint32_t)__cvta_generic_to_shared(Vs);
+  const uint32_t sQk = (uint32_t)__cvta_generic_to_shared(Qk), sDk = (uint32_t)__cvta_generic_to_shared(Dk);
+  const uint32_t sQm = (uint32_t)__cvta_generic_to_shared(Qm), sDm = (uint32_t)__cvta_generic_to_shared(Dm);
+  const uint32_t sPt = (uint32_t)__cvta_generic_to_shared(Pt), sSt = (uint32_t)__cvta_generic_to_shared(St);
+  constexpr uint32_t kColV = 128, kColK = 192;  // dV, dK accumulators
+  uint32_t phase = 0;
+  for (int64_t q0 = 0; q0 < a.s_real; q0 += kN) {
+    const int n = (int)(a.s_real - q0 < kN ? a.s_real - q0 : kN);
+    stage_rows<DKP>(a.q, a.ldq, h, a.dk, q0, n, Qk, Qm);
+    stage_rows<DVP>(a.dout, a.ldv, h, a.dv, q0, n, Dk, Dm);
+    {  // lse, delta of the block's queries (thread t: query q0 + t)
+      float l_ = 0.f, d_ = 0.f;
+      if (tid < n) {
+        const int64_t qr = q0 + tid;
+        l_ = a.lse[qr * a.H + h];
+        for (int t = 0; t < a.dv; ++t)
+          d_ += __bfloat162float(a.dout[qr * a.ldv + (int64_t)h * a.dv + t]) *
+                __bfloat162float(a.o[qr * a.ldv + (int64_t)h * a.dv + t]);
+      }
+      ls[tid] = l_;
+      dl[tid] = d_;
+    }
+    fence_async_smem();
+    tc_before_sync();
+    __syncthreads();
+    tc_after_sync();
+    if (tid == 0) {  // S^T = K Q^T
+#pragma unroll
+      for (int kc = 0; kc < DKP / 16; ++kc)
+        mma_bf16(tmem, smem_desc(sK + kc * 256, 128, DKP * 16), smem_desc(sQk + kc * 256, 128, DKP * 16),
+                 instr_desc(kM, kN), kc > 0);
+      mma_commit(bar);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    tc_after_sync();
+    float p[kN];
+#pragma unroll
+    for (int q4 = 0; q4 < kN / 32; ++q4) {
+      float v32[32];
+      tmem_ld32(t_row + q4 * 32, v32);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int c = q4 * 32 + i;
+        float x = fmaf(v32[i], a.scale_l, -ls[c]);
+        if (a.bias && real && c < n) x = fmaf(a.bias[(q0 + c) * a.S + key], 1.4426950408889634f, x);
+        p[c] = (real && c < n) ? ex2_approx(x) : 0.f;
+      }
+#pragma unroll
+      for (int c8 = 0; c8 < 4; ++c8) {
+        uint32_t w[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int c = q4 * 32 + c8 * 8 + 2 * i;
+          __nv_bfloat162 b2 = __floats2bfloat162_rn(p[c], p[c + 1]);
+          w[i] = *reinterpret_cast<uint32_t*>(&b2);
+        }
+        *reinterpret_cast<uint4*>(Pt + canon(tid, q4 * 32 + c8 * 8, kN)) = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+    }
+    tc_before_sync();
+    __syncthreads();
+    tc_after_sync();
+    if (tid == 0) {  // dP^T = V dO^T
+#pragma unroll
+      for (int kc = 0; kc < DVP / 16; ++kc)
+        mma_bf16(tmem, smem_desc(sV + kc * 256, 128, DVP * 16), smem_desc(sDk + kc * 256, 128, DVP * 16),
+                 instr_desc(kM, kN), kc > 0);
+      mma_commit(bar);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    tc_after_sync();
+#pragma unroll
+    for (int q4 = 0; q4 < kN / 32; ++q4) {
+      float v32[32];
+      tmem_ld32(t_row + q4 * 32, v32);
+#pragma unroll
+      for (int c8 = 0; c8 < 4; ++c8) {
+        uint32_t w[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int j = c8 * 8 + 2 * i, c = q4 * 32 + j;
+          const float d0 = p[c] * (v32[j] - dl[c]), d1 = p[c + 1] * (v32[j + 1] - dl[c + 1]);
+          __nv_bfloat162 b2 = __floats2bfloat162_rn(d0, d1);
+          w[i] = *reinterpret_cast<uint32_t*>(&b2);
+        }
+        *reinterpret_cast<uint4*>(St + canon(tid, q4 * 32 + c8 * 8, kN)) = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+    }
+    fence_async_smem();
+    tc_before_sync();
+    __syncthreads();
+    tc_after_sync();
+    if (tid == 0) {  // dV += P^T dO, dK += dS^T Q
+#pragma unroll
+      for (int kc = 0; kc < kN / 16; ++kc)
+        mma_bf16(tmem + kColV, smem_desc(sPt + kc * 256, 128, kN * 16), smem_desc(sDm + kc * 256, 128, 2048),
+                 instr_desc_bmn(kM, DVP), (q0 > 0 || kc > 0) ? 1u : 0u);
+#pragma unroll
+      for (int kc = 0; kc < kN / 16; ++kc)
+        mma_bf16(tmem + kColK, smem_desc(sSt + kc * 256, 128, kN * 16), smem_desc(sQm + kc * 256, 128, 2048),
+                 instr_desc_bmn(kM, DKP), (q0 > 0 || kc > 0) ? 1u : 0u);
+      mma_commit(bar);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    tc_after_sync();
+  }
+  if (key < a.S) {
+    if (real) {
+#pragma unroll
+      for (int q4 = 0; q4 < (DVP + 31) / 32; ++q4) {
+        float v32[32];
+        tmem_ld32(t_row + kColV + q4 * 32, v32);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int t = q4 * 32 + i;
+          if (t < a.dv) a.dv_out[key * a.ldv + (int64_t)h * a.dv + t] = __float2bfloat16(v32[i]);
+        }
+      }
+#pragma unroll
+      for (int q4 = 0; q4 < (DKP + 31) / 32; ++q4) {
+        float v32[32];
+        tmem_ld32(t_row + kColK + q4 * 32, v32);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int t = q4 * 32 + i;
+          if (t < a.dk) a.dk_out[key * a.ldq + (int64_t)h * a.dk + t] = __float2bfloat16(v32[i] * a.scale);
+        }
+      }
+    } else {  // pad column: only its own pad row attends, p = 1: dV = dO, dK = 0
+      for (int t = 0; t < a.dk; ++t) a.dk_out[key * a.ldq + (int64_t)h * a.dk + t] = bz();
+      for (int t = 0; t < a.dv; ++t)
+        a.dv_out[key * a.ldv + (int64_t)h * a.dv + t] = a.dout[key * a.ldv + (int64_t)h * a.dv + t];
+    }
+  }
+  tc_before_sync();
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+}
+
+template <int DKP, int DVP>
+cudaError_t launch_bwd(const TcBwdArgs& a, cudaStream_t st) {
+  const size_t s1 = (size_t)kM * (DKP + DVP) * 2 + (size_t)kN * (DKP + DVP) * 2 + (size_t)DKP * kN * 2 +
+                    (size_t)kM * kN * 2 + 16;
+  const size_t s2 = (size_t)kM * (DKP + DVP) * 2 + (size_t)kN * (DKP + DVP) * 2 + (size_t)(DKP + DVP) * kN * 2 +
+                    2 * (size_t)kM * kN * 2 + 2 * kN * 4 + 16;
+  cudaError_t e = cudaFuncSetAttribute(dense_tc_dq_kernel<DKP, DVP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)s1);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(dense_tc_dkdv_kernel<DKP, DVP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2);
+  if (e != cudaSuccess) return e;
+  dim3 grid((unsigned)((a.S + kM - 1) / kM), (unsigned)a.H);
+  dense_tc_dq_kernel<DKP, DVP><<<grid, kM, s1, st>>>(a);
+  dense_tc_dkdv_kernel<DKP, DVP><<<grid, kM, s2, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int DKP>
+cudaError_t launch_bwd_dv(const TcBwdArgs& a, cudaStream_t st) {
+  switch ((a.dv + 15) / 16 * 16) {
+    case 16: return launch_bwd<DKP, 16>(a, st);
+    case 32: return launch_bwd<DKP, 32>(a, st);
+    case 48: return launch_bwd<DKP, 48>(a, st);
+    default: return launch_bwd<DKP, 64>(a, st);
+  }
+}
 }  // namespace
 
 namespace gte_b200 {
@@ -379,6 +765,33 @@ cudaError_t launch_dense_tc_fwd(int64_t S, int64_t s_real, int H, int dk, int dv
     case 32: return launch_dv<32>(a, st);
     case 48: return launch_dv<48>(a, st);
     default: return launch_dv<64>(a, st);
+  }
+}
+
+// bf16 dense backward on tcgen05 (no weight_mult / dbias; dk, dv <= 64)
+cudaError_t launch_dense_tc_bwd(int64_t S, int64_t s_real, int H, int dk, int dv, const void* q, const void* k,
+                                int64_t ldq, const void* v, int64_t ldv, const void* out, const void* lse,
+                                const void* dout, const void* bias, void* dq, void* dk_out, void* dv_out,
+                                cudaStream_t st) {
+  TcBwdArgs a{};
+  a.S = S, a.s_real = s_real, a.H = H, a.dk = dk, a.dv = dv, a.ldq = ldq, a.ldv = ldv;
+  a.q = static_cast<const __nv_bfloat16*>(q);
+  a.k = static_cast<const __nv_bfloat16*>(k);
+  a.v = static_cast<const __nv_bfloat16*>(v);
+  a.o = static_cast<const __nv_bfloat16*>(out);
+  a.dout = static_cast<const __nv_bfloat16*>(dout);
+  a.bias = static_cast<const float*>(bias);
+  a.lse = static_cast<const float*>(lse);
+  a.dq = static_cast<__nv_bfloat16*>(dq);
+  a.dk_out = static_cast<__nv_bfloat16*>(dk_out);
+  a.dv_out = static_cast<__nv_bfloat16*>(dv_out);
+  a.scale = (float)(1.0 / std::sqrt((double)dk));
+  a.scale_l = (float)(1.4426950408889634 / std::sqrt((double)dk));
+  switch ((dk + 15) / 16 * 16) {
+    case 16: return launch_bwd_dv<16>(a, st);
+    case 32: return launch_bwd_dv<32>(a, st);
+    case 48: return launch_bwd_dv<48>(a, st);
+    default: return launch_bwd_dv<64>(a, st);
   }
 }
 

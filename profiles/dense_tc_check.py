@@ -28,3 +28,24 @@ for (S, s_real, H, dh) in CASES:
     print(f"S={S} s_real={s_real} H={H} dh={dh}: tc-vs-f32 max-norm err {e:.3e}, lse err {el:.3e}; tc fwd {t*1e3:.3f} ms "
           f"({pairs / t / 1e12:.2f} T pair-heads/s, {exps_bound / t * 100:.1f}% of the MUFU exp bound, "
           f"{4 * dh * pairs / t / 1e12:.1f} TFLOP/s algorithmic), cuda-core f32 fwd {t32*1e3:.3f} ms", flush=True)
+
+# backward (tcgen05 for bf16 without weight_mult / dbias) vs the CUDA-core f32 backward
+for (S, H, dh) in ((4096, 8, 8), (32768, 8, 8)):
+    g = torch.Generator(device="cuda").manual_seed(1)
+    q, k, v, up = (torch.randn((S, H * dh), generator=g, device="cuda").to(torch.bfloat16) for _ in range(4))
+    att = A.DeviceDenseAttention(S, H, dh, dh, "bf16")
+    o, lse = att.forward(q, k, v)
+    res = att.backward(q, k, v, o, lse, up)
+    att32 = A.DeviceDenseAttention(S, H, dh, dh, "f32")
+    o32, l32 = att32.forward(q.float(), k.float(), v.float())
+    r32 = att32.backward(q.float(), k.float(), v.float(), o32, l32, up.float())
+    torch.cuda.synchronize()
+    errs = [((a.float() - b).abs().max() / b.abs().max()).item() for a, b in zip(res[:3], r32[:3])]
+    def tm(fn, n=5):
+        fn(); torch.cuda.synchronize(); t0 = time.perf_counter()
+        for _ in range(n): fn()
+        torch.cuda.synchronize(); return (time.perf_counter() - t0) / n
+    t = tm(lambda: att.backward(q, k, v, o, lse, up))
+    t32 = tm(lambda: att32.backward(q.float(), k.float(), v.float(), o32, l32, up.float()), 2)
+    print(f"bwd S={S} H={H} dh={dh}: tc-vs-f32 max-norm err dq/dk/dv {errs[0]:.2e}/{errs[1]:.2e}/{errs[2]:.2e}; "
+          f"tc bwd {t*1e3:.3f} ms, cuda-core f32 bwd {t32*1e3:.3f} ms", flush=True)

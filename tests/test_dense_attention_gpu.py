@@ -125,3 +125,33 @@ def test_multihead_and_pad_rows_vs_oracle(cuda, orc, dtype, S, s_real, H, dh):
             sl = slice(h * dh, (h + 1) * dh)
             assert np.array_equal(f(out)[pad, sl], (wm[h][pad, pad][:, None] * vn[pad, sl]).astype(
                 np.float32 if dtype == "f32" else np.float64))
+
+
+@pytest.mark.parametrize("S,s_real,H,dh,with_bias", [(300, 300, 8, 8, False), (300, 257, 8, 8, True),
+                                                     (200, 200, 4, 16, True), (130, 130, 2, 24, False)])
+def test_tcgen05_backward_vs_oracle(cuda, orc, S, s_real, H, dh, with_bias):
+    """bf16 dense backward without weight_mult / dbias runs on tcgen05
+    (dense_tc.cu: dq and dkdv kernels): gradients vs the oracle over the
+    explicit dense execution pattern, bf16 tolerance."""
+    import torch
+
+    rng = np.random.default_rng(S + H + dh)
+    q, k, v, up = (rng.standard_normal((S, H * dh)) for _ in range(4))
+    bias = rng.normal(0, 0.3, (S, S)) if with_bias else None
+    tq, tk, tv, tu = (_dev(x, "bf16") for x in (q, k, v, up))
+    tb = _dev(bias, "f32") if with_bias else None
+    att = A.DeviceDenseAttention(S, H, dh, dh, "bf16", s_real=s_real)
+    out, lse = att.forward(tq, tk, tv, tb)
+    dq, dk, dv, _ = att.backward(tq, tk, tv, out, lse, tu, tb)
+    torch.cuda.synchronize()
+    f = lambda t: t.double().cpu().numpy()  # noqa: E731
+    qn, kn, vn, un = f(tq), f(tk), f(tv), f(tu)
+    g = _exec_pattern(S, s_real)
+    rows = np.repeat(np.arange(S), np.diff(g.row_off))
+    b_e = bias[rows, g.cols] if with_bias else None
+    for h in range(H):
+        sl = slice(h * dh, (h + 1) * dh)
+        a_, b_, c_, _ = orc.sparse_bwd(qn[:, sl], kn[:, sl], vn[:, sl], g, b_e, None, un[:, sl])
+        close(f(dq)[:, sl], a_, "bf16", f"dq h{h}")
+        close(f(dk)[:, sl], b_, "bf16", f"dk h{h}")
+        close(f(dv)[:, sl], c_, "bf16", f"dv h{h}")
