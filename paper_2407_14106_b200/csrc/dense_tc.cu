@@ -516,18 +516,21 @@ __global__ void __launch_bounds__(kM, 2) dense_tc_dq_kernel(TcBwdArgs a) {
     phase ^= 1;
     tc_after_sync();
   }
-  if (row < a.S) {
-    float g[DKP];
-    if (a.s_real > 0) {
+  // tcgen05.ld is warp-collective: every thread loads, only valid rows store
+  float g[DKP];
 #pragma unroll
-      for (int q4 = 0; q4 < (DKP + 31) / 32; ++q4) {
-        float v32[32];
-        tmem_ld32(t_row + 128 + q4 * 32, v32);
+  for (int t = 0; t < DKP; ++t) g[t] = 0.f;
+  if (a.s_real > 0) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (q4 * 32 + i < DKP) g[q4 * 32 + i] = v32[i];
-      }
+    for (int q4 = 0; q4 < (DKP + 31) / 32; ++q4) {
+      float v32[32];
+      tmem_ld32(t_row + 128 + q4 * 32, v32);
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (q4 * 32 + i < DKP) g[q4 * 32 + i] = v32[i];
     }
+  }
+  if (row < a.S) {
 #pragma unroll
     for (int t = 0; t < DKP; ++t)
       if (t < a.dk) a.dq[row * a.ldq + (int64_t)h * a.dk + t] = __float2bfloat16(real ? g[t] * a.scale : 0.f);
@@ -680,28 +683,30 @@ __global__ void __launch_bounds__(kM, 2) dense_tc_dkdv_kernel(TcBwdArgs a) {
     phase ^= 1;
     tc_after_sync();
   }
+  // tcgen05.ld is warp-collective: every thread loads, only valid keys store
+  const bool any_q = a.s_real > 0;
+#pragma unroll
+  for (int q4 = 0; q4 < (DVP + 31) / 32; ++q4) {
+    float v32[32];
+    if (any_q) tmem_ld32(t_row + kColV + q4 * 32, v32);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const int t = q4 * 32 + i;
+      if (real && t < a.dv) a.dv_out[key * a.ldv + (int64_t)h * a.dv + t] = __float2bfloat16(v32[i]);
+    }
+  }
+#pragma unroll
+  for (int q4 = 0; q4 < (DKP + 31) / 32; ++q4) {
+    float v32[32];
+    if (any_q) tmem_ld32(t_row + kColK + q4 * 32, v32);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const int t = q4 * 32 + i;
+      if (real && t < a.dk) a.dk_out[key * a.ldq + (int64_t)h * a.dk + t] = __float2bfloat16(v32[i] * a.scale);
+    }
+  }
   if (key < a.S) {
     if (real) {
-#pragma unroll
-      for (int q4 = 0; q4 < (DVP + 31) / 32; ++q4) {
-        float v32[32];
-        tmem_ld32(t_row + kColV + q4 * 32, v32);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const int t = q4 * 32 + i;
-          if (t < a.dv) a.dv_out[key * a.ldv + (int64_t)h * a.dv + t] = __float2bfloat16(v32[i]);
-        }
-      }
-#pragma unroll
-      for (int q4 = 0; q4 < (DKP + 31) / 32; ++q4) {
-        float v32[32];
-        tmem_ld32(t_row + kColK + q4 * 32, v32);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const int t = q4 * 32 + i;
-          if (t < a.dk) a.dk_out[key * a.ldq + (int64_t)h * a.dk + t] = __float2bfloat16(v32[i] * a.scale);
-        }
-      }
     } else {  // pad column: only its own pad row attends, p = 1: dV = dO, dK = 0
       for (int t = 0; t < a.dk; ++t) a.dk_out[key * a.ldq + (int64_t)h * a.dk + t] = bz();
       for (int t = 0; t < a.dv; ++t)
