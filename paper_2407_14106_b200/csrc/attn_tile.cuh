@@ -225,6 +225,47 @@ __device__ __forceinline__ void tile_own_rows(const TileMeta& mt, int nrows, con
   }
 }
 
+// Sum over the LPN lanes of a row of v[u] (u < EPL), recursive halving: after
+// min(log2 EPL, log2 LPN) stages each lane holds the partial sum of one edge
+// (index `which`); remaining stages are a plain butterfly. Lanes whose
+// `owner` flag is set store.
+template <int EPL, int LPN>
+struct EdgeReduce {
+  static constexpr int stages_split() {
+    int s = 0, n = EPL, g = LPN;
+    while (n > 1 && g > 1) { n >>= 1; g >>= 1; ++s; }
+    return s;
+  }
+  __device__ __forceinline__ static float run(float (&v)[EPL], int w, int& which, bool& owner) {
+    int n = EPL, base = 0;
+    int o = LPN / 2;
+#pragma unroll
+    for (int st = 0; st < stages_split(); ++st) {
+      const int half = n / 2;
+      const bool upper = (w & o) != 0;
+#pragma unroll
+      for (int t = 0; t < EPL / 2; ++t) {
+        if (t < half) {
+          const float send = upper ? v[t] : v[t + half];
+          const float keep = upper ? v[t + half] : v[t];
+          v[t] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+      }
+      if (upper) base += half;
+      n = half;
+      o >>= 1;
+    }
+    float x = v[0];
+#pragma unroll
+    for (; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    which = base;
+    // lanes sharing `which` after the butterfly: keep the one with low bits 0
+    constexpr int kRest = LPN >> stages_split();  // lanes per edge after the split
+    owner = (w & (kRest - 1)) == 0;
+    return x;
+  }
+};
+
 // ---------------------------------------------------------------------------
 // Forward: O, LSE (log2 units).
 template <typename T, int LPH, int LPN, int EPL, bool WM, bool HALO>
@@ -414,9 +455,15 @@ __global__ void __launch_bounds__(kTileThreads, HALO ? 2 : GTE_TILE_MINB) tile_b
       ob = d = 0;
     }
   };
+  // delta = dO_i . O_i per head; warp-uniform call (head_sum shuffles)
+  auto row_delta = [&](bool fresh) {
+    const float x = head_sum<LPH>(P::dot(dd, oo));
+    if (fresh) delta = x;
+  };
   {
     const int r0 = (threadIdx.x >> 5) * SLOTS + g.slot;
     start_row(r0 < nrows ? r0 : -1);
+    row_delta(true);
   }
 
   while (__any_sync(0xffffffffu, i >= 0)) {
@@ -439,10 +486,10 @@ __global__ void __launch_bounds__(kTileThreads, HALO ? 2 : GTE_TILE_MINB) tile_b
       }
     }
     const bool single = d == 1;
-    // delta = dO_i . O_i (first step of the row); degree-1 rows take the dw
-    // of their edge so ds == 0 exactly in both passes (attention.cpp:265-272)
-    const float dot_do = head_sum<LPH>(P::dot(dd, oo));
-    if (k == 0) delta = dot_do;
+    // delta = dO_i . O_i is set at row start (row_delta); degree-1 rows take
+    // the dw of their edge so ds == 0 exactly in both passes
+    // (attention.cpp:265-272)
+    float hs[EPL];
 #pragma unroll
     for (int u = 0; u < EPL; ++u) {
       const float sc = head_sum<LPH>(P::dot(q, kr[u]));
@@ -452,11 +499,23 @@ __global__ void __launch_bounds__(kTileThreads, HALO ? 2 : GTE_TILE_MINB) tile_b
       if (u == 0 && single && k == 0) delta = dw;
       const float ds = (u < rem && !single) ? pr * (dw - delta) : 0.f;
       P::axpy(ds, kr[u], dq);
-      // dbias_e = sum over heads (parallel.cpp:319): one contribution per head
-      float hsum = (g.part == 0 && g.head_ok) ? ds : 0.f;
+      hs[u] = (g.part == 0 && g.head_ok) ? ds : 0.f;  // one contribution per head
+    }
+    if (DB) {  // dbias_e = sum over heads (parallel.cpp:319)
+      if constexpr (LPN >= EPL) {  // recursive halving: EPL sums leave the slot's lanes at once
+        int which;
+        bool owner;
+        const float tot = EdgeReduce<EPL, LPN>::run(hs, g.lane % LPN, which, owner);
+        if (owner && i >= 0 && which < rem) DB[gb + k + which] = tot;
+      } else {
 #pragma unroll
-      for (int off = LPH; off < LPN; off <<= 1) hsum += __shfl_xor_sync(0xffffffffu, hsum, off);
-      if (DB && u < rem && (g.lane % LPN) == 0) DB[gb + k + u] = hsum;
+        for (int u = 0; u < EPL; ++u) {
+          float hsum = hs[u];
+#pragma unroll
+          for (int off = 1; off < LPN; off <<= 1) hsum += __shfl_xor_sync(0xffffffffu, hsum, off);
+          if (i >= 0 && u < rem && (g.lane % LPN) == 0) DB[gb + k + u] = hsum;
+        }
+      }
     }
     k += EPL;
     const bool done = i >= 0 && k >= d;
@@ -470,6 +529,7 @@ __global__ void __launch_bounds__(kTileThreads, HALO ? 2 : GTE_TILE_MINB) tile_b
       }
       const int nr = rq_.refill(done, g.lane);
       if (done) start_row(nr);
+      row_delta(done);
     }
   }
 }

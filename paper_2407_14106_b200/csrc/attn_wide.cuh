@@ -146,47 +146,6 @@ __device__ __forceinline__ WideGeom wide_geom() {
   return g;
 }
 
-// Sum over the LPN lanes of a row of v[u] (u < EPL), recursive halving: after
-// min(log2 EPL, log2 LPN) stages each lane holds the partial sum of one edge
-// (index `which`); remaining stages are a plain butterfly. Lanes whose
-// `owner` flag is set store.
-template <int EPL, int LPN>
-struct EdgeReduce {
-  static constexpr int stages_split() {
-    int s = 0, n = EPL, g = LPN;
-    while (n > 1 && g > 1) { n >>= 1; g >>= 1; ++s; }
-    return s;
-  }
-  __device__ __forceinline__ static float run(float (&v)[EPL], int w, int& which, bool& owner) {
-    int n = EPL, base = 0;
-    int o = LPN / 2;
-#pragma unroll
-    for (int st = 0; st < stages_split(); ++st) {
-      const int half = n / 2;
-      const bool upper = (w & o) != 0;
-#pragma unroll
-      for (int t = 0; t < EPL / 2; ++t) {
-        if (t < half) {
-          const float send = upper ? v[t] : v[t + half];
-          const float keep = upper ? v[t + half] : v[t];
-          v[t] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-        }
-      }
-      if (upper) base += half;
-      n = half;
-      o >>= 1;
-    }
-    float x = v[0];
-#pragma unroll
-    for (; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-    which = base;
-    // lanes sharing `which` after the butterfly: keep the one with low bits 0
-    constexpr int kRest = LPN >> stages_split();  // lanes per edge after the split
-    owner = (w & (kRest - 1)) == 0;
-    return x;
-  }
-};
-
 // Per-tile metadata of the wide kernels (padded offsets + real degrees).
 struct WideMeta {
   int row[kTileRows];
