@@ -342,3 +342,22 @@ def test_fwd_bwd_host_matches_device_path(cuda, dtype):
         att.fwd_bwd_host(hq, hk, hv, hdo, hb, *outs, hdb)
     for got, nm in zip(outs + [hdb], ("out", "dq", "dk", "dv", "db")):
         assert np.array_equal(got.double().numpy(), r[nm]), nm
+
+
+@pytest.mark.parametrize("dtype,which", [("f32", 0), ("bf16", 0), ("f32", 1), ("bf16", 2)])
+def test_non_finite_multihead_tile_path(cuda, dtype, which):
+    """attention.cpp:20-22 on the tile kernels: a NaN/inf anywhere in Q, K or V
+    (here in a row that is some tile's own row) raises DataError at sync."""
+    import torch
+
+    ro, co = community_graph(3000, 8.0, community=64, seed=2)
+    td = _torch_dtype(dtype)
+    q, k, v = (torch.randn((3000, 64), device="cuda").to(td) for _ in range(3))
+    [q, k, v][which][1234, 17] = float("nan") if which != 1 else float("inf")
+    plan = A.DevicePlan.from_host(ro, co)
+    att = A.DeviceSparseAttention(plan, 8, 8, 8, dtype)
+    att.forward(q, k, v)
+    with pytest.raises(DataError, match=f"non-finite {'QKV'[which]}"):
+        plan.ctx.sync()
+    att.forward(*(torch.randn((3000, 64), device="cuda").to(td) for _ in range(3)))
+    plan.ctx.sync()  # the error latch was reset
