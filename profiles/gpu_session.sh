@@ -12,10 +12,10 @@ if [[ $WHAT == all || $WHAT == tests ]]; then
   tail -3 $O/pytest_gpu_${TAG}.log
 fi
 if [[ $WHAT == all || $WHAT == bench ]]; then
-  timeout 900 python bench.py > $O/bench_f32_${TAG}.log 2>&1; echo "rc=$?" >> $O/bench_f32_${TAG}.log
-  timeout 600 python bench.py --dtype bf16 --no-cpu-baseline > $O/bench_bf16_${TAG}.log 2>&1; echo "rc=$?" >> $O/bench_bf16_${TAG}.log
+  timeout 900 python bench.py > $O/bench_default_${TAG}.log 2>&1; echo "rc=$?" >> $O/bench_default_${TAG}.log
+  timeout 600 python bench.py --dtype f32 --no-cpu-baseline > $O/bench_f32_${TAG}.log 2>&1; echo "rc=$?" >> $O/bench_f32_${TAG}.log
   timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_ref_${TAG}.log 2>&1; echo "rc=$?" >> $O/bench_ref_${TAG}.log
-  tail -2 $O/bench_f32_${TAG}.log $O/bench_bf16_${TAG}.log
+  tail -n 2 $O/bench_default_${TAG}.log
 fi
 if [[ $WHAT == all || $WHAT == ncu ]]; then
   timeout 900 bash profiles/ncu_capture.sh f32 $TAG > $O/ncu_f32_${TAG}.log 2>&1
