@@ -118,6 +118,28 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -128,20 +150,31 @@ __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.a
 __device__ __forceinline__ void tc_before_sync() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_after_sync() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
-template <int DKP, int DVP>
-__global__ void __launch_bounds__(kM, 4) dense_tc_fwd_kernel(TcArgs a) {
+// 8 warps per 128-row tile: warps w and w + 4 share TMEM lane quadrant w & 3
+// (rows 32 (w & 3) ..) and split the 128 key columns in halves; row maxima
+// and sums combine through shared memory; each half accumulates half of the
+// output columns. Twice the warps of a 4-warp tile at the same TMEM budget
+// (128 columns per CTA, 4 CTAs per SM), for latency hiding.
+template <int DKP, int DVP, bool BW>  // BW: a bias or a weight_mult is present
+__global__ void __launch_bounds__(2 * kM, 3) dense_tc_fwd_kernel(TcArgs a) {
+  constexpr int kT = 2 * kM;     // threads
+  constexpr int kHalfN = kN / 2; // key columns per thread
+  constexpr int kHalfV = DVP / 2;
   extern __shared__ __align__(1024) unsigned char smem[];
   unsigned char* Qs = smem;                       // [128 x DKP]
   unsigned char* Ks = Qs + kM * DKP * 2;          // [128 x DKP]
   unsigned char* Vt = Ks + kN * DKP * 2;          // [DVP x 128]
   unsigned char* Ps = Vt + DVP * kN * 2;          // [128 x 128]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(Ps + kM * kN * 2);
+  float* red = reinterpret_cast<float*>(Ps + kM * kN * 2);  // [2][128] partial maxima / sums
+  uint64_t* bar = reinterpret_cast<uint64_t*>(red + 2 * kM);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
 
-  const int tid = threadIdx.x, warp = tid >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int quad = warp & 3, half = warp >> 2;
+  const int rl = quad * 32 + lane;  // row within the tile (= TMEM lane)
   const int h = blockIdx.y;
   const int64_t r0 = (int64_t)blockIdx.x * kM;
-  const int64_t row = r0 + tid;
+  const int64_t row = r0 + rl;
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(
@@ -152,8 +185,7 @@ __global__ void __launch_bounds__(kM, 4) dense_tc_fwd_kernel(TcArgs a) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  // stage Q (rows >= s_real: zeros; they are handled by the epilogue)
-  for (int x = tid; x < kM * DKP; x += kM) {
+  for (int x = tid; x < kM * DKP; x += kT) {
     const int r = x / DKP, kk = x % DKP;
     const int64_t gr = r0 + r;
     __nv_bfloat16 val = __float2bfloat16(0.f);
@@ -164,29 +196,29 @@ __global__ void __launch_bounds__(kM, 4) dense_tc_fwd_kernel(TcArgs a) {
   __syncthreads();
   tc_after_sync();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t t_row = tmem + ((uint32_t)(warp * 32) << 16);  // this warp's 32 lanes
+  const uint32_t t_row = tmem + ((uint32_t)(quad * 32) << 16);
   const uint32_t sQ = (uint32_t)__cvta_generic_to_shared(Qs), sK = (uint32_t)__cvta_generic_to_shared(Ks);
   const uint32_t sV = (uint32_t)__cvta_generic_to_shared(Vt), sP = (uint32_t)__cvta_generic_to_shared(Ps);
   constexpr uint32_t kIdS = instr_desc(kM, kN), kIdO = instr_desc(kM, DVP);
 
-  float m = -INFINITY, l = 0.f, acc[DVP];
+  float m = -INFINITY, l = 0.f, acc[kHalfV];
 #pragma unroll
-  for (int t = 0; t < DVP; ++t) acc[t] = 0.f;
+  for (int t = 0; t < kHalfV; ++t) acc[t] = 0.f;
   uint32_t phase = 0;
   const bool real = row < a.s_real;
+  const int cbase = half * kHalfN;
 
   for (int64_t c0 = 0; c0 < a.s_real; c0 += kN) {
     const int n = (int)(a.s_real - c0 < kN ? a.s_real - c0 : kN);
-    // 1. stage K block and V^T block
-    if (a.vec) {  // one 16-byte chunk (8 elements) per thread and step
-      for (int x = tid; x < kN * (DKP / 8); x += kM) {
+    if (a.vec) {
+      for (int x = tid; x < kN * (DKP / 8); x += kT) {
         const int c = x / (DKP / 8), kk = (x % (DKP / 8)) * 8;
         uint4 val = make_uint4(0, 0, 0, 0);
         if (c < n && kk < a.dk)
           val = __ldg(reinterpret_cast<const uint4*>(a.k + (c0 + c) * a.ldq + (int64_t)h * a.dk + kk));
         *reinterpret_cast<uint4*>(Ks + canon(c, kk, DKP)) = val;
       }
-      for (int x = tid; x < kN * (DVP / 8); x += kM) {
+      for (int x = tid; x < kN * (DVP / 8); x += kT) {
         const int c = x / (DVP / 8), t0 = (x % (DVP / 8)) * 8;
         uint4 val = make_uint4(0, 0, 0, 0);
         if (c < n && t0 < a.dv)
@@ -196,13 +228,13 @@ __global__ void __launch_bounds__(kM, 4) dense_tc_fwd_kernel(TcArgs a) {
         for (int t = 0; t < 8; ++t) *reinterpret_cast<__nv_bfloat16*>(Vt + canon(t0 + t, c, kN)) = e8[t];
       }
     } else {
-      for (int x = tid; x < kN * DKP; x += kM) {
+      for (int x = tid; x < kN * DKP; x += kT) {
         const int c = x / DKP, kk = x % DKP;
         __nv_bfloat16 val = __float2bfloat16(0.f);
         if (c < n && kk < a.dk) val = a.k[(c0 + c) * a.ldq + (int64_t)h * a.dk + kk];
         *reinterpret_cast<__nv_bfloat16*>(Ks + canon(c, kk, DKP)) = val;
       }
-      for (int x = tid; x < kN * DVP; x += kM) {
+      for (int x = tid; x < kN * DVP; x += kT) {
         const int c = x / DVP, t = x % DVP;
         __nv_bfloat16 val = __float2bfloat16(0.f);
         if (c < n && t < a.dv) val = a.v[(c0 + c) * a.ldv + (int64_t)h * a.dv + t];
@@ -213,7 +245,6 @@ __global__ void __launch_bounds__(kM, 4) dense_tc_fwd_kernel(TcArgs a) {
     tc_before_sync();
     __syncthreads();
     tc_after_sync();
-    // 2. S = Q K^T
     if (tid == 0) {
 #pragma unroll
       for (int kc = 0; kc < DKP / 16; ++kc)
@@ -224,53 +255,49 @@ __global__ void __launch_bounds__(kM, 4) dense_tc_fwd_kernel(TcArgs a) {
     mbar_wait(bar, phase);
     phase ^= 1;
     tc_after_sync();
-    // 3. online softmax on this thread's row, two passes over TMEM (max, then
-    //    p): 32 scores live at a time keeps the CTA at ~100 registers. Without
-    //    a bias the scale folds into one FFMA per score: max(scale*s) =
-    //    scale*max(s) (scale > 0), p = ex2(s*scale - m).
+    // pass 1: this thread's half-row maximum, combined with the partner's
     float mx = -INFINITY;
 #pragma unroll
-    for (int q4 = 0; q4 < kN / 32; ++q4) {
-      float v32[32];
-      tmem_ld32(t_row + q4 * 32, v32);
-      if (a.bias) {
+    for (int q4 = 0; q4 < kHalfN / 16; ++q4) {
+      float v16[16];
+      tmem_ld16(t_row + cbase + q4 * 16, v16);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const int c = q4 * 32 + i;
-          float x = v32[i] * a.scale_l;
+      for (int i = 0; i < 16; ++i) {
+        const int c = cbase + q4 * 16 + i;
+        float x = v16[i];
+        if (BW && a.bias) {
+          x *= a.scale_l;
           if (real && c < n) x = fmaf(a.bias[row * a.S + c0 + c], 1.4426950408889634f, x);
-          mx = fmaxf(mx, c < n ? x : -INFINITY);
         }
-      } else if (q4 * 32 + 32 <= n) {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) mx = fmaxf(mx, v32[i]);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) mx = fmaxf(mx, q4 * 32 + i < n ? v32[i] : -INFINITY);
+        mx = fmaxf(mx, c < n ? x : -INFINITY);
       }
     }
-    if (!a.bias) mx *= a.scale_l;
+    if (!(BW && a.bias)) mx *= a.scale_l;
+    red[half * kM + rl] = mx;
+    __syncthreads();
+    mx = fmaxf(red[rl], red[kM + rl]);
     const float mn = fmaxf(m, mx);
     const float corr = ex2_approx(m - mn);
     l *= corr;
+    // pass 2: p for this half-row -> P (bf16), partial row sum
 #pragma unroll
-    for (int q4 = 0; q4 < kN / 32; ++q4) {
-      float v32[32];
-      tmem_ld32(t_row + q4 * 32, v32);
+    for (int q4 = 0; q4 < kHalfN / 16; ++q4) {
+      float v32[16];
+      tmem_ld16(t_row + cbase + q4 * 16, v32);
 #pragma unroll
-      for (int c8 = 0; c8 < 4; ++c8) {
+      for (int c8 = 0; c8 < 2; ++c8) {
         uint32_t w[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const int j = c8 * 8 + 2 * i, c = q4 * 32 + j;
+          const int j = c8 * 8 + 2 * i, c = cbase + q4 * 16 + j;
           float x0 = fmaf(v32[j], a.scale_l, -mn), x1 = fmaf(v32[j + 1], a.scale_l, -mn);
-          if (a.bias && real) {
+          if (BW && a.bias && real) {
             if (c < n) x0 = fmaf(a.bias[row * a.S + c0 + c], 1.4426950408889634f, x0);
             if (c + 1 < n) x1 = fmaf(a.bias[row * a.S + c0 + c + 1], 1.4426950408889634f, x1);
           }
           float p0 = c < n ? ex2_approx(x0) : 0.f, p1 = c + 1 < n ? ex2_approx(x1) : 0.f;
           l += p0 + p1;
-          if (a.wmult && real) {
+          if (BW && a.wmult && real) {
             const float* wr = a.wmult + ((int64_t)h * a.S + row) * a.S + c0;
             p0 = c < n ? p0 * wr[c] : 0.f;
             p1 = c + 1 < n ? p1 * wr[c + 1] : 0.f;
@@ -278,7 +305,8 @@ __global__ void __launch_bounds__(kM, 4) dense_tc_fwd_kernel(TcArgs a) {
           __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
           w[i] = *reinterpret_cast<uint32_t*>(&b2);
         }
-        *reinterpret_cast<uint4*>(Ps + canon(tid, q4 * 32 + c8 * 8, kN)) = make_uint4(w[0], w[1], w[2], w[3]);
+        *reinterpret_cast<uint4*>(Ps + canon(rl, cbase + q4 * 16 + c8 * 8, kN)) =
+            make_uint4(w[0], w[1], w[2], w[3]);
       }
     }
     m = mn;
@@ -286,7 +314,6 @@ __global__ void __launch_bounds__(kM, 4) dense_tc_fwd_kernel(TcArgs a) {
     tc_before_sync();
     __syncthreads();
     tc_after_sync();
-    // 4. O_blk = P V into TMEM columns [0, DVP)
     if (tid == 0) {
 #pragma unroll
       for (int kc = 0; kc < kN / 16; ++kc)
@@ -296,29 +323,33 @@ __global__ void __launch_bounds__(kM, 4) dense_tc_fwd_kernel(TcArgs a) {
     mbar_wait(bar, phase);
     phase ^= 1;
     tc_after_sync();
-    // 5. acc = acc * corr + O_blk
+    // this half's output columns [half * DVP/2, (half + 1) * DVP/2)
 #pragma unroll
-    for (int q4 = 0; q4 < (DVP + 31) / 32; ++q4) {
-      float v32[32];
-      tmem_ld32(t_row + q4 * 32, v32);
+    for (int c8 = 0; c8 < kHalfV / 8; ++c8) {
+      float v8[8];
+      tmem_ld8(t_row + half * kHalfV + c8 * 8, v8);
 #pragma unroll
-      for (int i = 0; i < 32; ++i)
-        if (q4 * 32 + i < DVP) acc[q4 * 32 + i] = fmaf(acc[q4 * 32 + i], corr, v32[i]);
+      for (int i = 0; i < 8; ++i) acc[c8 * 8 + i] = fmaf(acc[c8 * 8 + i], corr, v8[i]);
     }
     tc_before_sync();
     __syncthreads();
     tc_after_sync();
   }
-  // epilogue
+  // epilogue: row sum = both halves' partial sums
+  red[half * kM + rl] = l;
+  __syncthreads();
+  const float lt = red[rl] + red[kM + rl];
   if (row < a.S) {
     if (real) {
-      const float inv = 1.f / l;
+      const float inv = 1.f / lt;
 #pragma unroll
-      for (int t = 0; t < DVP; ++t)
-        if (t < a.dv) a.out[row * a.ldv + (int64_t)h * a.dv + t] = __float2bfloat16(acc[t] * inv);
-      a.lse[row * a.H + h] = m + log2f(l);
-    } else {  // pad row: attends only itself (model.cpp:400-403)
-      const float mult = a.wmult ? a.wmult[((int64_t)h * a.S + row) * a.S + row] : 1.f;
+      for (int t = 0; t < kHalfV; ++t) {
+        const int col = half * kHalfV + t;
+        if (col < a.dv) a.out[row * a.ldv + (int64_t)h * a.dv + col] = __float2bfloat16(acc[t] * inv);
+      }
+      if (half == 0) a.lse[row * a.H + h] = m + log2f(lt);
+    } else if (half == 0) {  // pad row: attends only itself (model.cpp:400-403)
+      const float mult = (BW && a.wmult) ? a.wmult[((int64_t)h * a.S + row) * a.S + row] : 1.f;
       for (int t = 0; t < a.dv; ++t) {
         const float vv = __bfloat162float(a.v[row * a.ldv + (int64_t)h * a.dv + t]);
         a.out[row * a.ldv + (int64_t)h * a.dv + t] = __float2bfloat16(mult * vv);
@@ -333,12 +364,20 @@ __global__ void __launch_bounds__(kM, 4) dense_tc_fwd_kernel(TcArgs a) {
 
 template <int DKP, int DVP>
 cudaError_t launch(const TcArgs& a, cudaStream_t st) {
-  const size_t smem = (size_t)kM * DKP * 2 + (size_t)kN * DKP * 2 + (size_t)DVP * kN * 2 + (size_t)kM * kN * 2 + 16;
-  cudaError_t e = cudaFuncSetAttribute(dense_tc_fwd_kernel<DKP, DVP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
-  if (e != cudaSuccess) return e;
+  const size_t smem = (size_t)kM * DKP * 2 + (size_t)kN * DKP * 2 + (size_t)DVP * kN * 2 + (size_t)kM * kN * 2 +
+                      2 * kM * sizeof(float) + 16;
   dim3 grid((unsigned)((a.S + kM - 1) / kM), (unsigned)a.H);
-  dense_tc_fwd_kernel<DKP, DVP><<<grid, kM, smem, st>>>(a);
+  if (a.bias || a.wmult) {
+    cudaError_t e = cudaFuncSetAttribute(dense_tc_fwd_kernel<DKP, DVP, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    dense_tc_fwd_kernel<DKP, DVP, true><<<grid, 2 * kM, smem, st>>>(a);
+  } else {
+    cudaError_t e = cudaFuncSetAttribute(dense_tc_fwd_kernel<DKP, DVP, false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    dense_tc_fwd_kernel<DKP, DVP, false><<<grid, 2 * kM, smem, st>>>(a);
+  }
   return cudaGetLastError();
 }
 
