@@ -438,8 +438,41 @@ __device__ __forceinline__ void stage_rows(const __nv_bfloat16* g, int64_t ld, i
   }
 }
 
+// Both backward kernels run 8 warps per 128-row tile: warps w and w + 4 share
+// TMEM lane quadrant w & 3 and split the 128 columns of S / dP (no row
+// reductions are needed in the backward: lse and delta are per row / column
+// inputs); the accumulators' columns are split between the two halves.
+constexpr int kBT = 2 * kM;  // threads of the backward kernels
+
+// stage rows [r0, r0+n) of a [S x (H*W)] bf16 tensor, head h, W valid of WP
+// columns, as a K-major [128 x WP] tile and (optionally) an MN-major
+// [WP x 128] tile (row index = k)
+template <int WP>
+__device__ __forceinline__ void stage_rows8(const __nv_bfloat16* g, int64_t ld, int h, int W, int64_t r0, int n,
+                                            unsigned char* kmaj, unsigned char* mnmaj) {
+  for (int x = threadIdx.x; x < 128 * WP; x += kBT) {
+    const int r = x / WP, c = x % WP;
+    const __nv_bfloat16 val = (r < n && c < W) ? g[(r0 + r) * ld + (int64_t)h * W + c] : bz();
+    if (kmaj) *reinterpret_cast<__nv_bfloat16*>(kmaj + canon(r, c, WP)) = val;
+    if (mnmaj) *reinterpret_cast<__nv_bfloat16*>(mnmaj + canon_mn(r, c)) = val;
+  }
+}
+
+// columns [c0, c0 + NC) of this thread's TMEM lane -> v (NC multiple of 8)
+template <int NC>
+__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, float (&v)[NC]) {
+#pragma unroll
+  for (int c8 = 0; c8 < NC / 8; ++c8) {
+    float x[8];
+    tmem_ld8(taddr + c8 * 8, x);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[c8 * 8 + i] = x[i];
+  }
+}
+
 template <int DKP, int DVP>
-__global__ void __launch_bounds__(kM, 2) dense_tc_dq_kernel(TcBwdArgs a) {
+__global__ void __launch_bounds__(kBT, 2) dense_tc_dq_kernel(TcBwdArgs a) {
+  constexpr int kHN = kN / 2, kHK = DKP / 2;
   extern __shared__ __align__(1024) unsigned char smem[];
   unsigned char* Qs = smem;                    // [128 x DKP] K-major (A of S)
   unsigned char* Ds = Qs + kM * DKP * 2;       // [128 x DVP] K-major (A of dP)
@@ -449,8 +482,9 @@ __global__ void __launch_bounds__(kM, 2) dense_tc_dq_kernel(TcBwdArgs a) {
   unsigned char* dS = Km + DKP * kN * 2;       // [128 x 128] K-major (A of dQ)
   uint64_t* bar = reinterpret_cast<uint64_t*>(dS + kM * kN * 2);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
-  const int tid = threadIdx.x, warp = tid >> 5, h = blockIdx.y;
-  const int64_t r0 = (int64_t)blockIdx.x * kM, row = r0 + tid;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, quad = warp & 3, half = warp >> 2;
+  const int rl = quad * 32 + lane, cb = half * kHN, h = blockIdx.y;
+  const int64_t r0 = (int64_t)blockIdx.x * kM, row = r0 + rl;
   const bool real = row < a.s_real;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
@@ -462,8 +496,8 @@ __global__ void __launch_bounds__(kM, 2) dense_tc_dq_kernel(TcBwdArgs a) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   const int nq = (int)(a.s_real - r0 < kM ? (a.s_real - r0 > 0 ? a.s_real - r0 : 0) : kM);
-  stage_rows<DKP>(a.q, a.ldq, h, a.dk, r0, nq, Qs, nullptr);
-  stage_rows<DVP>(a.dout, a.ldv, h, a.dv, r0, nq, Ds, nullptr);
+  stage_rows8<DKP>(a.q, a.ldq, h, a.dk, r0, nq, Qs, nullptr);
+  stage_rows8<DVP>(a.dout, a.ldv, h, a.dv, r0, nq, Ds, nullptr);
   float lse = 0.f, delta = 0.f;
   if (real) {
     lse = a.lse[row * a.H + h];
@@ -474,15 +508,15 @@ __global__ void __launch_bounds__(kM, 2) dense_tc_dq_kernel(TcBwdArgs a) {
   tc_before_sync();
   __syncthreads();
   tc_after_sync();
-  const uint32_t tmem = *tmem_slot, t_row = tmem + ((uint32_t)(warp * 32) << 16);
+  const uint32_t tmem = *tmem_slot, t_row = tmem + ((uint32_t)(quad * 32) << 16);
   const uint32_t sQ = (uint32_t)__cvta_generic_to_shared(Qs), sD = (uint32_t)__cvta_generic_to_shared(Ds);
   const uint32_t sK = (uint32_t)__cvta_generic_to_shared(Ks), sV = (uint32_t)__cvta_generic_to_shared(Vs);
   const uint32_t sKm = (uint32_t)__cvta_generic_to_shared(Km), sS = (uint32_t)__cvta_generic_to_shared(dS);
   uint32_t phase = 0;
   for (int64_t c0 = 0; c0 < a.s_real; c0 += kN) {
     const int n = (int)(a.s_real - c0 < kN ? a.s_real - c0 : kN);
-    stage_rows<DKP>(a.k, a.ldq, h, a.dk, c0, n, Ks, Km);
-    stage_rows<DVP>(a.v, a.ldv, h, a.dv, c0, n, Vs, nullptr);
+    stage_rows8<DKP>(a.k, a.ldq, h, a.dk, c0, n, Ks, Km);
+    stage_rows8<DVP>(a.v, a.ldv, h, a.dv, c0, n, Vs, nullptr);
     fence_async_smem();
     tc_before_sync();
     __syncthreads();
@@ -497,17 +531,17 @@ __global__ void __launch_bounds__(kM, 2) dense_tc_dq_kernel(TcBwdArgs a) {
     mbar_wait(bar, phase);
     phase ^= 1;
     tc_after_sync();
-    float p[kN];
+    float p[kHN];
 #pragma unroll
-    for (int q4 = 0; q4 < kN / 32; ++q4) {
-      float v32[32];
-      tmem_ld32(t_row + q4 * 32, v32);
+    for (int q4 = 0; q4 < kHN / 16; ++q4) {
+      float v16[16];
+      tmem_ld16(t_row + cb + q4 * 16, v16);
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const int c = q4 * 32 + i;
-        float x = fmaf(v32[i], a.scale_l, -lse);
+      for (int i = 0; i < 16; ++i) {
+        const int c = cb + q4 * 16 + i;
+        float x = fmaf(v16[i], a.scale_l, -lse);
         if (a.bias && real && c < n) x = fmaf(a.bias[row * a.S + c0 + c], 1.4426950408889634f, x);
-        p[c] = (real && c < n) ? ex2_approx(x) : 0.f;
+        p[q4 * 16 + i] = (real && c < n) ? ex2_approx(x) : 0.f;
       }
     }
     tc_before_sync();
@@ -524,20 +558,20 @@ __global__ void __launch_bounds__(kM, 2) dense_tc_dq_kernel(TcBwdArgs a) {
     phase ^= 1;
     tc_after_sync();
 #pragma unroll
-    for (int q4 = 0; q4 < kN / 32; ++q4) {
-      float v32[32];
-      tmem_ld32(t_row + q4 * 32, v32);
+    for (int q4 = 0; q4 < kHN / 16; ++q4) {
+      float v16[16];
+      tmem_ld16(t_row + cb + q4 * 16, v16);
 #pragma unroll
-      for (int c8 = 0; c8 < 4; ++c8) {
+      for (int c8 = 0; c8 < 2; ++c8) {
         uint32_t w[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const int j = c8 * 8 + 2 * i, c = q4 * 32 + j;
-          const float d0 = p[c] * (v32[j] - delta), d1 = p[c + 1] * (v32[j + 1] - delta);
+          const int j = c8 * 8 + 2 * i, pc = q4 * 16 + j;
+          const float d0 = p[pc] * (v16[j] - delta), d1 = p[pc + 1] * (v16[j + 1] - delta);
           __nv_bfloat162 b2 = __floats2bfloat162_rn(d0, d1);
           w[i] = *reinterpret_cast<uint32_t*>(&b2);
         }
-        *reinterpret_cast<uint4*>(dS + canon(tid, q4 * 32 + c8 * 8, kN)) = make_uint4(w[0], w[1], w[2], w[3]);
+        *reinterpret_cast<uint4*>(dS + canon(rl, cb + q4 * 16 + c8 * 8, kN)) = make_uint4(w[0], w[1], w[2], w[3]);
       }
     }
     fence_async_smem();
@@ -556,23 +590,16 @@ __global__ void __launch_bounds__(kM, 2) dense_tc_dq_kernel(TcBwdArgs a) {
     tc_after_sync();
   }
   // tcgen05.ld is warp-collective: every thread loads, only valid rows store
-  float g[DKP];
+  float g[kHK];
 #pragma unroll
-  for (int t = 0; t < DKP; ++t) g[t] = 0.f;
-  if (a.s_real > 0) {
-#pragma unroll
-    for (int q4 = 0; q4 < (DKP + 31) / 32; ++q4) {
-      float v32[32];
-      tmem_ld32(t_row + 128 + q4 * 32, v32);
-#pragma unroll
-      for (int i = 0; i < 32; ++i)
-        if (q4 * 32 + i < DKP) g[q4 * 32 + i] = v32[i];
-    }
-  }
+  for (int t = 0; t < kHK; ++t) g[t] = 0.f;
+  if (a.s_real > 0) tmem_ld_cols<kHK>(t_row + 128 + half * kHK, g);
   if (row < a.S) {
 #pragma unroll
-    for (int t = 0; t < DKP; ++t)
-      if (t < a.dk) a.dq[row * a.ldq + (int64_t)h * a.dk + t] = __float2bfloat16(real ? g[t] * a.scale : 0.f);
+    for (int t = 0; t < kHK; ++t) {
+      const int col = half * kHK + t;
+      if (col < a.dk) a.dq[row * a.ldq + (int64_t)h * a.dk + col] = __float2bfloat16(real ? g[t] * a.scale : 0.f);
+    }
   }
   tc_before_sync();
   __syncthreads();
@@ -580,7 +607,8 @@ __global__ void __launch_bounds__(kM, 2) dense_tc_dq_kernel(TcBwdArgs a) {
 }
 
 template <int DKP, int DVP>
-__global__ void __launch_bounds__(kM, 2) dense_tc_dkdv_kernel(TcBwdArgs a) {
+__global__ void __launch_bounds__(kBT, 2) dense_tc_dkdv_kernel(TcBwdArgs a) {
+  constexpr int kHN = kN / 2, kHK = DKP / 2, kHV = DVP / 2;
   extern __shared__ __align__(1024) unsigned char smem[];
   unsigned char* Ks = smem;                    // [128 keys x DKP] K-major (A of S^T)
   unsigned char* Vs = Ks + kM * DKP * 2;       // [128 keys x DVP] K-major (A of dP^T)
@@ -594,8 +622,9 @@ __global__ void __launch_bounds__(kM, 2) dense_tc_dkdv_kernel(TcBwdArgs a) {
   float* dl = ls + kN;                                     // [128] delta of the query block
   uint64_t* bar = reinterpret_cast<uint64_t*>(dl + kN);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
-  const int tid = threadIdx.x, warp = tid >> 5, h = blockIdx.y;
-  const int64_t k0 = (int64_t)blockIdx.x * kM, key = k0 + tid;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, quad = warp & 3, half = warp >> 2;
+  const int rl = quad * 32 + lane, cb = half * kHN, h = blockIdx.y;
+  const int64_t k0 = (int64_t)blockIdx.x * kM, key = k0 + rl;
   const bool real = key < a.s_real;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
@@ -607,12 +636,12 @@ __global__ void __launch_bounds__(kM, 2) dense_tc_dkdv_kernel(TcBwdArgs a) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   const int nk = (int)(a.s_real - k0 < kM ? (a.s_real - k0 > 0 ? a.s_real - k0 : 0) : kM);
-  stage_rows<DKP>(a.k, a.ldq, h, a.dk, k0, nk, Ks, nullptr);
-  stage_rows<DVP>(a.v, a.ldv, h, a.dv, k0, nk, Vs, nullptr);
+  stage_rows8<DKP>(a.k, a.ldq, h, a.dk, k0, nk, Ks, nullptr);
+  stage_rows8<DVP>(a.v, a.ldv, h, a.dv, k0, nk, Vs, nullptr);
   tc_before_sync();
   __syncthreads();
   tc_after_sync();
-  const uint32_t tmem = *tmem_slot, t_row = tmem + ((uint32_t)(warp * 32) << 16);
+  const uint32_t tmem = *tmem_slot, t_row = tmem + ((uint32_t)(quad * 32) << 16);
   const uint32_t sK = (uint32_t)__cvta_generic_to_shared(Ks), sV = (uint32_t)__cvta_generic_to_shared(Vs);
   const uint32_t sQk = (uint32_t)__cvta_generic_to_shared(Qk), sDk = (uint32_t)__cvta_generic_to_shared(Dk);
   const uint32_t sQm = (uint32_t)__cvta_generic_to_shared(Qm), sDm = (uint32_t)__cvta_generic_to_shared(Dm);
@@ -621,9 +650,9 @@ __global__ void __launch_bounds__(kM, 2) dense_tc_dkdv_kernel(TcBwdArgs a) {
   uint32_t phase = 0;
   for (int64_t q0 = 0; q0 < a.s_real; q0 += kN) {
     const int n = (int)(a.s_real - q0 < kN ? a.s_real - q0 : kN);
-    stage_rows<DKP>(a.q, a.ldq, h, a.dk, q0, n, Qk, Qm);
-    stage_rows<DVP>(a.dout, a.ldv, h, a.dv, q0, n, Dk, Dm);
-    {  // lse, delta of the block's queries (thread t: query q0 + t)
+    stage_rows8<DKP>(a.q, a.ldq, h, a.dk, q0, n, Qk, Qm);
+    stage_rows8<DVP>(a.dout, a.ldv, h, a.dv, q0, n, Dk, Dm);
+    if (tid < kN) {  // lse, delta of the block's queries (thread t: query q0 + t)
       float l_ = 0.f, d_ = 0.f;
       if (tid < n) {
         const int64_t qr = q0 + tid;
@@ -649,28 +678,28 @@ __global__ void __launch_bounds__(kM, 2) dense_tc_dkdv_kernel(TcBwdArgs a) {
     mbar_wait(bar, phase);
     phase ^= 1;
     tc_after_sync();
-    float p[kN];
+    float p[kHN];
 #pragma unroll
-    for (int q4 = 0; q4 < kN / 32; ++q4) {
-      float v32[32];
-      tmem_ld32(t_row + q4 * 32, v32);
+    for (int q4 = 0; q4 < kHN / 16; ++q4) {
+      float v16[16];
+      tmem_ld16(t_row + cb + q4 * 16, v16);
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const int c = q4 * 32 + i;
-        float x = fmaf(v32[i], a.scale_l, -ls[c]);
+      for (int i = 0; i < 16; ++i) {
+        const int c = cb + q4 * 16 + i;
+        float x = fmaf(v16[i], a.scale_l, -ls[c]);
         if (a.bias && real && c < n) x = fmaf(a.bias[(q0 + c) * a.S + key], 1.4426950408889634f, x);
-        p[c] = (real && c < n) ? ex2_approx(x) : 0.f;
+        p[q4 * 16 + i] = (real && c < n) ? ex2_approx(x) : 0.f;
       }
 #pragma unroll
-      for (int c8 = 0; c8 < 4; ++c8) {
+      for (int c8 = 0; c8 < 2; ++c8) {
         uint32_t w[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const int c = q4 * 32 + c8 * 8 + 2 * i;
-          __nv_bfloat162 b2 = __floats2bfloat162_rn(p[c], p[c + 1]);
+          const int pc = q4 * 16 + c8 * 8 + 2 * i;
+          __nv_bfloat162 b2 = __floats2bfloat162_rn(p[pc], p[pc + 1]);
           w[i] = *reinterpret_cast<uint32_t*>(&b2);
         }
-        *reinterpret_cast<uint4*>(Pt + canon(tid, q4 * 32 + c8 * 8, kN)) = make_uint4(w[0], w[1], w[2], w[3]);
+        *reinterpret_cast<uint4*>(Pt + canon(rl, cb + q4 * 16 + c8 * 8, kN)) = make_uint4(w[0], w[1], w[2], w[3]);
       }
     }
     tc_before_sync();
@@ -687,20 +716,20 @@ __global__ void __launch_bounds__(kM, 2) dense_tc_dkdv_kernel(TcBwdArgs a) {
     phase ^= 1;
     tc_after_sync();
 #pragma unroll
-    for (int q4 = 0; q4 < kN / 32; ++q4) {
-      float v32[32];
-      tmem_ld32(t_row + q4 * 32, v32);
+    for (int q4 = 0; q4 < kHN / 16; ++q4) {
+      float v16[16];
+      tmem_ld16(t_row + cb + q4 * 16, v16);
 #pragma unroll
-      for (int c8 = 0; c8 < 4; ++c8) {
+      for (int c8 = 0; c8 < 2; ++c8) {
         uint32_t w[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const int j = c8 * 8 + 2 * i, c = q4 * 32 + j;
-          const float d0 = p[c] * (v32[j] - dl[c]), d1 = p[c + 1] * (v32[j + 1] - dl[c + 1]);
+          const int j = c8 * 8 + 2 * i, pc = q4 * 16 + j, c = cb + pc;
+          const float d0 = p[pc] * (v16[j] - dl[c]), d1 = p[pc + 1] * (v16[j + 1] - dl[c + 1]);
           __nv_bfloat162 b2 = __floats2bfloat162_rn(d0, d1);
           w[i] = *reinterpret_cast<uint32_t*>(&b2);
         }
-        *reinterpret_cast<uint4*>(St + canon(tid, q4 * 32 + c8 * 8, kN)) = make_uint4(w[0], w[1], w[2], w[3]);
+        *reinterpret_cast<uint4*>(St + canon(rl, cb + q4 * 16 + c8 * 8, kN)) = make_uint4(w[0], w[1], w[2], w[3]);
       }
     }
     fence_async_smem();
@@ -724,33 +753,30 @@ __global__ void __launch_bounds__(kM, 2) dense_tc_dkdv_kernel(TcBwdArgs a) {
   }
   // tcgen05.ld is warp-collective: every thread loads, only valid keys store
   const bool any_q = a.s_real > 0;
+  float gv[kHV], gk[kHK];
 #pragma unroll
-  for (int q4 = 0; q4 < (DVP + 31) / 32; ++q4) {
-    float v32[32];
-    if (any_q) tmem_ld32(t_row + kColV + q4 * 32, v32);
+  for (int t = 0; t < kHV; ++t) gv[t] = 0.f;
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const int t = q4 * 32 + i;
-      if (real && t < a.dv) a.dv_out[key * a.ldv + (int64_t)h * a.dv + t] = __float2bfloat16(v32[i]);
-    }
+  for (int t = 0; t < kHK; ++t) gk[t] = 0.f;
+  if (any_q) {
+    tmem_ld_cols<kHV>(t_row + kColV + half * kHV, gv);
+    tmem_ld_cols<kHK>(t_row + kColK + half * kHK, gk);
   }
+  if (real) {
 #pragma unroll
-  for (int q4 = 0; q4 < (DKP + 31) / 32; ++q4) {
-    float v32[32];
-    if (any_q) tmem_ld32(t_row + kColK + q4 * 32, v32);
+    for (int t = 0; t < kHV; ++t) {
+      const int col = half * kHV + t;
+      if (col < a.dv) a.dv_out[key * a.ldv + (int64_t)h * a.dv + col] = __float2bfloat16(gv[t]);
+    }
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const int t = q4 * 32 + i;
-      if (real && t < a.dk) a.dk_out[key * a.ldq + (int64_t)h * a.dk + t] = __float2bfloat16(v32[i] * a.scale);
+    for (int t = 0; t < kHK; ++t) {
+      const int col = half * kHK + t;
+      if (col < a.dk) a.dk_out[key * a.ldq + (int64_t)h * a.dk + col] = __float2bfloat16(gk[t] * a.scale);
     }
-  }
-  if (key < a.S) {
-    if (real) {
-    } else {  // pad column: only its own pad row attends, p = 1: dV = dO, dK = 0
-      for (int t = 0; t < a.dk; ++t) a.dk_out[key * a.ldq + (int64_t)h * a.dk + t] = bz();
-      for (int t = 0; t < a.dv; ++t)
-        a.dv_out[key * a.ldv + (int64_t)h * a.dv + t] = a.dout[key * a.ldv + (int64_t)h * a.dv + t];
-    }
+  } else if (key < a.S && half == 0) {  // pad column: only its own pad row attends, p = 1: dV = dO, dK = 0
+    for (int t = 0; t < a.dk; ++t) a.dk_out[key * a.ldq + (int64_t)h * a.dk + t] = bz();
+    for (int t = 0; t < a.dv; ++t)
+      a.dv_out[key * a.ldv + (int64_t)h * a.dv + t] = a.dout[key * a.ldv + (int64_t)h * a.dv + t];
   }
   tc_before_sync();
   __syncthreads();
@@ -769,8 +795,8 @@ cudaError_t launch_bwd(const TcBwdArgs& a, cudaStream_t st) {
   e = cudaFuncSetAttribute(dense_tc_dkdv_kernel<DKP, DVP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2);
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)((a.S + kM - 1) / kM), (unsigned)a.H);
-  dense_tc_dq_kernel<DKP, DVP><<<grid, kM, s1, st>>>(a);
-  dense_tc_dkdv_kernel<DKP, DVP><<<grid, kM, s2, st>>>(a);
+  dense_tc_dq_kernel<DKP, DVP><<<grid, kBT, s1, st>>>(a);
+  dense_tc_dkdv_kernel<DKP, DVP><<<grid, kBT, s2, st>>>(a);
   return cudaGetLastError();
 }
 
