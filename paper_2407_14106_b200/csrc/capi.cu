@@ -120,6 +120,7 @@ struct gte_ctx {
   int* h_err = nullptr;  // pinned mirror
   int64_t launches = 0;
   DevBuf io[13];  // [11] delta (generic), [12] packed (lse, delta) (tile)
+  DevBuf scratch;  // workspace of other translation units (ctx_scratch)
 };
 
 struct gte_plan {
@@ -667,6 +668,7 @@ int gte_ctx_destroy(gte_ctx* c) {
     for (auto& e : c->ev) cudaEventDestroy(e);
   }
   for (auto& b : c->io) b.release();
+  c->scratch.release();
   cudaFree(c->d_err);
   cudaFreeHost(c->h_err);
   delete c;
@@ -1032,6 +1034,8 @@ namespace gte_b200 {
 int set_error(int code, const std::string& msg) { return fail(code, msg); }
 int64_t& ctx_launch_counter(gte_ctx* c) { return c->launches; }
 void* ctx_stream(gte_ctx* c) { return (void*)c->stream; }
+// grow-only device workspace owned by the context (stream-ordered use only)
+void* ctx_scratch(gte_ctx* c, size_t bytes) { return c->scratch.ensure(bytes) == cudaSuccess ? c->scratch.p : nullptr; }
 
 cudaError_t launch_finite_rows(int dtype, const void* k, const void* v, const int32_t* rows, int nrows,
                                int64_t ldq, int64_t ldv, int64_t wq, int64_t wv, int* err, cudaStream_t st) {

@@ -39,7 +39,8 @@ cudaError_t launch_dense_tc_fwd(int64_t S, int64_t s_real, int H, int dk, int dv
 cudaError_t launch_dense_tc_bwd(int64_t S, int64_t s_real, int H, int dk, int dv, const void* q, const void* k,
                                 int64_t ldq, const void* v, int64_t ldv, const void* out, const void* lse,
                                 const void* dout, const void* bias, void* dq, void* dk_out, void* dv_out,
-                                cudaStream_t st);
+                                float* delta_ws, cudaStream_t st);
+void* ctx_scratch(gte_ctx* c, size_t bytes);
 int set_error(int code, const std::string& msg);
 int64_t& ctx_launch_counter(gte_ctx* c);
 void* ctx_stream(gte_ctx* c);
@@ -473,7 +474,10 @@ int gte_dense_attn_bwd(gte_ctx* ctx, int dtype, int64_t S, int64_t s_real, int H
     return !(e && e[0] == '0');
   }();
   if (dtype == GTE_BF16 && tc && !wmult && !dbias) {
-    DCUDA(launch_dense_tc_bwd(S, s_real, H, dk, dv, q, k, ldq, v, ldv, out, lse, dout, bias, dq, dk_out, dv_out, st));
+    float* ws = static_cast<float*>(ctx_scratch(ctx, sizeof(float) * (size_t)S * H));
+    if (!ws) return set_error(GTE_CUDA, "dense_attention_backward: workspace allocation failed");
+    DCUDA(launch_dense_tc_bwd(S, s_real, H, dk, dv, q, k, ldq, v, ldv, out, lse, dout, bias, dq, dk_out, dv_out, ws,
+                              st));
     ctx_launch_counter(ctx) += 2;
     return GTE_OK;
   }

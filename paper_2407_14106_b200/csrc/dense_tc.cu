@@ -419,7 +419,9 @@ struct TcBwdArgs {
   const float* bias;  // [S*S] or null (score input only)
   const float* lse;   // [S*H] log2 units (forward)
   __nv_bfloat16 *dq, *dk_out, *dv_out;
+  float* delta;  // [S*H] workspace: written by the dq kernel, read by dkdv
   float scale_l, scale;
+  int vec;  // 16-byte chunk staging (dk, dv multiples of 8, 16-byte aligned rows)
 };
 
 __device__ __forceinline__ __nv_bfloat16 bz() { return __float2bfloat16(0.f); }
@@ -449,7 +451,17 @@ constexpr int kBT = 2 * kM;  // threads of the backward kernels
 // [WP x 128] tile (row index = k)
 template <int WP>
 __device__ __forceinline__ void stage_rows8(const __nv_bfloat16* g, int64_t ld, int h, int W, int64_t r0, int n,
-                                            unsigned char* kmaj, unsigned char* mnmaj) {
+                                            unsigned char* kmaj, unsigned char* mnmaj, int vec) {
+  if (vec) {  // one 16-byte chunk (8 elements) per step; both layouts take it as one 16-byte store
+    for (int x = threadIdx.x; x < 128 * (WP / 8); x += kBT) {
+      const int r = x / (WP / 8), c = (x % (WP / 8)) * 8;
+      uint4 val = make_uint4(0, 0, 0, 0);
+      if (r < n && c < W) val = __ldg(reinterpret_cast<const uint4*>(g + (r0 + r) * ld + (int64_t)h * W + c));
+      if (kmaj) *reinterpret_cast<uint4*>(kmaj + canon(r, c, WP)) = val;
+      if (mnmaj) *reinterpret_cast<uint4*>(mnmaj + canon_mn(r, c)) = val;
+    }
+    return;
+  }
   for (int x = threadIdx.x; x < 128 * WP; x += kBT) {
     const int r = x / WP, c = x % WP;
     const __nv_bfloat16 val = (r < n && c < W) ? g[(r0 + r) * ld + (int64_t)h * W + c] : bz();
@@ -496,14 +508,15 @@ __global__ void __launch_bounds__(kBT, 2) dense_tc_dq_kernel(TcBwdArgs a) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   const int nq = (int)(a.s_real - r0 < kM ? (a.s_real - r0 > 0 ? a.s_real - r0 : 0) : kM);
-  stage_rows8<DKP>(a.q, a.ldq, h, a.dk, r0, nq, Qs, nullptr);
-  stage_rows8<DVP>(a.dout, a.ldv, h, a.dv, r0, nq, Ds, nullptr);
+  stage_rows8<DKP>(a.q, a.ldq, h, a.dk, r0, nq, Qs, nullptr, a.vec);
+  stage_rows8<DVP>(a.dout, a.ldv, h, a.dv, r0, nq, Ds, nullptr, a.vec);
   float lse = 0.f, delta = 0.f;
   if (real) {
     lse = a.lse[row * a.H + h];
     for (int t = 0; t < a.dv; ++t)
       delta += __bfloat162float(a.dout[row * a.ldv + (int64_t)h * a.dv + t]) *
                __bfloat162float(a.o[row * a.ldv + (int64_t)h * a.dv + t]);
+    if (half == 0) a.delta[row * a.H + h] = delta;  // for the dkdv kernel
   }
   tc_before_sync();
   __syncthreads();
@@ -515,8 +528,8 @@ __global__ void __launch_bounds__(kBT, 2) dense_tc_dq_kernel(TcBwdArgs a) {
   uint32_t phase = 0;
   for (int64_t c0 = 0; c0 < a.s_real; c0 += kN) {
     const int n = (int)(a.s_real - c0 < kN ? a.s_real - c0 : kN);
-    stage_rows8<DKP>(a.k, a.ldq, h, a.dk, c0, n, Ks, Km);
-    stage_rows8<DVP>(a.v, a.ldv, h, a.dv, c0, n, Vs, nullptr);
+    stage_rows8<DKP>(a.k, a.ldq, h, a.dk, c0, n, Ks, Km, a.vec);
+    stage_rows8<DVP>(a.v, a.ldv, h, a.dv, c0, n, Vs, nullptr, a.vec);
     fence_async_smem();
     tc_before_sync();
     __syncthreads();
@@ -636,8 +649,8 @@ __global__ void __launch_bounds__(kBT, 2) dense_tc_dkdv_kernel(TcBwdArgs a) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   const int nk = (int)(a.s_real - k0 < kM ? (a.s_real - k0 > 0 ? a.s_real - k0 : 0) : kM);
-  stage_rows8<DKP>(a.k, a.ldq, h, a.dk, k0, nk, Ks, nullptr);
-  stage_rows8<DVP>(a.v, a.ldv, h, a.dv, k0, nk, Vs, nullptr);
+  stage_rows8<DKP>(a.k, a.ldq, h, a.dk, k0, nk, Ks, nullptr, a.vec);
+  stage_rows8<DVP>(a.v, a.ldv, h, a.dv, k0, nk, Vs, nullptr, a.vec);
   tc_before_sync();
   __syncthreads();
   tc_after_sync();
@@ -650,16 +663,14 @@ __global__ void __launch_bounds__(kBT, 2) dense_tc_dkdv_kernel(TcBwdArgs a) {
   uint32_t phase = 0;
   for (int64_t q0 = 0; q0 < a.s_real; q0 += kN) {
     const int n = (int)(a.s_real - q0 < kN ? a.s_real - q0 : kN);
-    stage_rows8<DKP>(a.q, a.ldq, h, a.dk, q0, n, Qk, Qm);
-    stage_rows8<DVP>(a.dout, a.ldv, h, a.dv, q0, n, Dk, Dm);
+    stage_rows8<DKP>(a.q, a.ldq, h, a.dk, q0, n, Qk, Qm, a.vec);
+    stage_rows8<DVP>(a.dout, a.ldv, h, a.dv, q0, n, Dk, Dm, a.vec);
     if (tid < kN) {  // lse, delta of the block's queries (thread t: query q0 + t)
       float l_ = 0.f, d_ = 0.f;
       if (tid < n) {
         const int64_t qr = q0 + tid;
         l_ = a.lse[qr * a.H + h];
-        for (int t = 0; t < a.dv; ++t)
-          d_ += __bfloat162float(a.dout[qr * a.ldv + (int64_t)h * a.dv + t]) *
-                __bfloat162float(a.o[qr * a.ldv + (int64_t)h * a.dv + t]);
+        d_ = a.delta[qr * a.H + h];  // dq kernel's dO . O
       }
       ls[tid] = l_;
       dl[tid] = d_;
@@ -842,7 +853,7 @@ cudaError_t launch_dense_tc_fwd(int64_t S, int64_t s_real, int H, int dk, int dv
 cudaError_t launch_dense_tc_bwd(int64_t S, int64_t s_real, int H, int dk, int dv, const void* q, const void* k,
                                 int64_t ldq, const void* v, int64_t ldv, const void* out, const void* lse,
                                 const void* dout, const void* bias, void* dq, void* dk_out, void* dv_out,
-                                cudaStream_t st) {
+                                float* delta_ws, cudaStream_t st) {
   TcBwdArgs a{};
   a.S = S, a.s_real = s_real, a.H = H, a.dk = dk, a.dv = dv, a.ldq = ldq, a.ldv = ldv;
   a.q = static_cast<const __nv_bfloat16*>(q);
@@ -857,6 +868,10 @@ cudaError_t launch_dense_tc_bwd(int64_t S, int64_t s_real, int H, int dk, int dv
   a.dv_out = static_cast<__nv_bfloat16*>(dv_out);
   a.scale = (float)(1.0 / std::sqrt((double)dk));
   a.scale_l = (float)(1.4426950408889634 / std::sqrt((double)dk));
+  a.vec = dk % 8 == 0 && dv % 8 == 0 && (ldq * 2) % 16 == 0 && (ldv * 2) % 16 == 0 &&
+          (reinterpret_cast<uintptr_t>(q) % 16) == 0 && (reinterpret_cast<uintptr_t>(k) % 16) == 0 &&
+          (reinterpret_cast<uintptr_t>(v) % 16) == 0 && (reinterpret_cast<uintptr_t>(dout) % 16) == 0;
+  a.delta = delta_ws;  // [S*H] floats, the context's workspace
   switch ((dk + 15) / 16 * 16) {
     case 16: return launch_bwd_dv<16>(a, st);
     case 32: return launch_bwd_dv<32>(a, st);
