@@ -121,6 +121,14 @@ int gte_sparse_attn_fwd_bwd_host(gte_ctx* ctx, const gte_plan* plan, int dtype, 
                                  int dv, const void* q, const void* k, const void* v,
                                  const void* dout, const void* bias, void* out, void* dq,
                                  void* dk_out, void* dv_out, void* dbias);
+/* asynchronous twin: returns once the step is enqueued (uploads, kernels and
+ * downloads on separate streams); consecutive steps overlap one step's
+ * downloads with the next one's uploads. Host buffers must stay untouched
+ * until gte_ctx_sync(), which waits for every enqueued step. */
+int gte_sparse_attn_fwd_bwd_host_async(gte_ctx* ctx, const gte_plan* plan, int dtype, int H, int dk,
+                                 int dv, const void* q, const void* k, const void* v,
+                                 const void* dout, const void* bias, void* out, void* dq,
+                                 void* dk_out, void* dv_out, void* dbias);
 
 /* ---- graph builders (device int32 CSR, bit-exact with the reference) ----
  * graph_from_edges   proj/src/graph.cpp:49-66  (range check -> DataError, sort, unique)

@@ -89,6 +89,7 @@ def lib() -> C.CDLL:
                                                    VP, VP]
             L.gte_sparse_attn_fwd_bwd_host.argtypes = [VP, VP, I32, I32, I32, I32, VP, VP, VP, VP, VP, VP, VP, VP,
                                                        VP, VP]
+            L.gte_sparse_attn_fwd_bwd_host_async.argtypes = L.gte_sparse_attn_fwd_bwd_host.argtypes
             _lib = L
     return _lib
 

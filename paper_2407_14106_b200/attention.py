@@ -376,16 +376,20 @@ class DeviceSparseAttention:
             dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), dbias.data_ptr()))
         return dq, dk, dv, dbias
 
-    def fwd_bwd_host(self, q, k, v, dout, bias, out, dq, dk, dv, dbias):
+    def fwd_bwd_host(self, q, k, v, dout, bias, out, dq, dk, dv, dbias, sync: bool = True):
         """End-to-end unit with host (ideally pinned) buffers: H2D, fwd, bwd, D2H.
-        Arguments are CPU tensors/arrays exposing .data_ptr() or ctypes."""
+        Arguments are CPU tensors/arrays exposing .data_ptr() or ctypes.
+        sync=False enqueues the step and returns (gte_sparse_attn_fwd_bwd_host_async):
+        consecutive steps overlap downloads with the next uploads; call
+        plan.ctx.sync() before reading the outputs."""
         def p(x):
             if x is None:
                 return None
             return x.data_ptr() if hasattr(x, "data_ptr") else x.ctypes.data
 
         self._stream()
-        check(_lib.lib().gte_sparse_attn_fwd_bwd_host(
+        fn = _lib.lib().gte_sparse_attn_fwd_bwd_host if sync else _lib.lib().gte_sparse_attn_fwd_bwd_host_async
+        check(fn(
             self.plan.ctx.h, self.plan.h, self.code, self.H, self.dk, self.dv, p(q), p(k), p(v), p(dout), p(bias),
             p(out), p(dq), p(dk), p(dv), p(dbias)))
 

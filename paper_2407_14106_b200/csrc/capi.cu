@@ -114,8 +114,11 @@ unsigned grid_for(int64_t n, int block = 256) {
 struct gte_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
-  cudaStream_t copy = nullptr;          // host<->device copies of the *_host entries (lazy)
-  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaStream_t copy = nullptr;          // host->device copies of the *_host entries (lazy)
+  cudaStream_t down = nullptr;          // device->host copies (lazy; its own copy engine direction)
+  cudaEvent_t ev[8] = {};               // [0] inputs in, [1] dO in, [2] O ready, [3] grads ready,
+                                        // [4] O read back, [5] grads read back, [6] scratch
+  bool pending = false;                 // a previous fwd_bwd_host step is still in flight
   int* d_err = nullptr;  // [0] non-finite bits, [1] first empty row
   int* h_err = nullptr;  // pinned mirror
   int64_t launches = 0;
@@ -664,7 +667,9 @@ int gte_ctx_destroy(gte_ctx* c) {
   cudaStreamSynchronize(c->stream);
   if (c->copy) {
     cudaStreamSynchronize(c->copy);
+    cudaStreamSynchronize(c->down);
     cudaStreamDestroy(c->copy);
+    cudaStreamDestroy(c->down);
     for (auto& e : c->ev) cudaEventDestroy(e);
   }
   for (auto& b : c->io) b.release();
@@ -680,7 +685,13 @@ int gte_ctx_set_stream(gte_ctx* c, void* s) {
   return GTE_OK;
 }
 
-int gte_ctx_sync(gte_ctx* c) { return drain_errors(c); }
+int gte_ctx_sync(gte_ctx* c) {
+  if (c->down) {  // in-flight asynchronous fwd_bwd_host steps
+    CUDA_TRY(cudaStreamSynchronize(c->down));
+    c->pending = false;
+  }
+  return drain_errors(c);
+}
 
 int64_t gte_ctx_launches(const gte_ctx* c) { return c->launches; }
 
@@ -974,58 +985,88 @@ int gte_sparse_attn_bwd_host(gte_ctx* c, const gte_plan* plan, int dtype, int H,
   return rc;
 }
 
-int gte_sparse_attn_fwd_bwd_host(gte_ctx* c, const gte_plan* plan, int dtype, int H, int dk, int dv,
-                                 const void* q, const void* k, const void* v, const void* dout,
-                                 const void* bias, void* out, void* dq, void* dk_out, void* dv_out,
-                                 void* dbias) {
+// One fwd+bwd unit with host buffers. Three streams: uploads (c->copy),
+// kernels (c->stream), downloads (c->down), ordered by events; dO travels
+// while the forward runs, O comes back while the backward runs. The async
+// variant returns after enqueueing: the next step's uploads then overlap this
+// step's downloads (each engine direction busy at once); gte_ctx_sync waits.
+static int fwd_bwd_host_impl(gte_ctx* c, const gte_plan* plan, int dtype, int H, int dk, int dv, const void* q,
+                             const void* k, const void* v, const void* dout, const void* bias, void* out, void* dq,
+                             void* dk_out, void* dv_out, void* dbias, bool sync) {
   int rc = check_attn_args(plan, dtype, H, dk, dv, (int64_t)H * dk, (int64_t)H * dv);
   if (rc) return rc;
   const size_t S = (size_t)plan->rows, E = (size_t)plan->nnz, es = elem_size(dtype), as = acc_size(dtype);
   const size_t bq = S * H * dk * es, bv = S * H * dv * es;
   cudaStream_t st = c->stream;
+  if (!c->copy) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->down, cudaStreamNonBlocking));
+    for (auto& e : c->ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  const bool grow = c->io[0].cap < bq || c->io[2].cap < bv || c->io[4].cap < S * H * as ||
+                    c->io[5].cap < (E + 1) * as || c->io[6].cap < (E + 1) * as;
+  if (grow && c->pending) {  // buffers are about to move: finish the step in flight first
+    CUDA_TRY(cudaStreamSynchronize(c->down));
+    c->pending = false;
+  }
   for (int i : {0, 1, 7, 8}) CUDA_TRY(c->io[i].ensure(bq));
   for (int i : {2, 3, 9, 10}) CUDA_TRY(c->io[i].ensure(bv));
   CUDA_TRY(c->io[4].ensure(S * H * as));
   CUDA_TRY(c->io[5].ensure((E + 1) * as));
   CUDA_TRY(c->io[6].ensure((E + 1) * as));
-  // copies on a second stream, ordered against the kernels with events: dO
-  // travels while the forward runs, O comes back while the backward runs
-  if (!c->copy) {
-    CUDA_TRY(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
-    for (auto& e : c->ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  }
-  cudaStream_t cp = c->copy;
-  CUDA_TRY(cudaEventRecord(c->ev[3], st));  // earlier work on the compute stream (buffers free)
-  CUDA_TRY(cudaStreamWaitEvent(cp, c->ev[3], 0));
-  CUDA_TRY(cudaMemcpyAsync(c->io[1].p, k, bq, cudaMemcpyHostToDevice, cp));
-  CUDA_TRY(cudaMemcpyAsync(c->io[2].p, v, bv, cudaMemcpyHostToDevice, cp));
-  CUDA_TRY(cudaMemcpyAsync(c->io[0].p, q, bq, cudaMemcpyHostToDevice, cp));
-  if (bias) CUDA_TRY(cudaMemcpyAsync(c->io[6].p, bias, E * as, cudaMemcpyHostToDevice, cp));
-  CUDA_TRY(cudaEventRecord(c->ev[0], cp));  // forward inputs resident
-  CUDA_TRY(cudaMemcpyAsync(c->io[9].p, dout, bv, cudaMemcpyHostToDevice, cp));
-  CUDA_TRY(cudaEventRecord(c->ev[1], cp));  // dO resident
+  cudaStream_t up = c->copy, dn = c->down;
+  // inputs may be overwritten once the previous step's kernels are done with them
+  CUDA_TRY(cudaEventRecord(c->ev[6], st));
+  CUDA_TRY(cudaStreamWaitEvent(up, c->ev[6], 0));
+  CUDA_TRY(cudaMemcpyAsync(c->io[1].p, k, bq, cudaMemcpyHostToDevice, up));
+  CUDA_TRY(cudaMemcpyAsync(c->io[2].p, v, bv, cudaMemcpyHostToDevice, up));
+  CUDA_TRY(cudaMemcpyAsync(c->io[0].p, q, bq, cudaMemcpyHostToDevice, up));
+  if (bias) CUDA_TRY(cudaMemcpyAsync(c->io[6].p, bias, E * as, cudaMemcpyHostToDevice, up));
+  CUDA_TRY(cudaEventRecord(c->ev[0], up));  // forward inputs resident
+  CUDA_TRY(cudaMemcpyAsync(c->io[9].p, dout, bv, cudaMemcpyHostToDevice, up));
+  CUDA_TRY(cudaEventRecord(c->ev[1], up));  // dO resident
   const void* bias_dev = bias ? c->io[6].p : nullptr;
   CUDA_TRY(cudaStreamWaitEvent(st, c->ev[0], 0));
+  if (c->pending) CUDA_TRY(cudaStreamWaitEvent(st, c->ev[4], 0));  // previous O read back
   rc = gte_sparse_attn_fwd(c, plan, dtype, H, dk, dv, c->io[0].p, c->io[1].p, (int64_t)H * dk, c->io[2].p,
                            (int64_t)H * dv, bias_dev, nullptr, c->io[3].p, c->io[4].p, 0);
   if (rc) return rc;
   CUDA_TRY(cudaEventRecord(c->ev[2], st));  // O ready
-  CUDA_TRY(cudaStreamWaitEvent(cp, c->ev[2], 0));
-  CUDA_TRY(cudaMemcpyAsync(out, c->io[3].p, bv, cudaMemcpyDeviceToHost, cp));
+  CUDA_TRY(cudaStreamWaitEvent(dn, c->ev[2], 0));
+  CUDA_TRY(cudaMemcpyAsync(out, c->io[3].p, bv, cudaMemcpyDeviceToHost, dn));
+  CUDA_TRY(cudaEventRecord(c->ev[4], dn));  // O read back
   CUDA_TRY(cudaStreamWaitEvent(st, c->ev[1], 0));
+  if (c->pending) CUDA_TRY(cudaStreamWaitEvent(st, c->ev[5], 0));  // previous gradients read back
   rc = gte_sparse_attn_bwd(c, plan, dtype, H, dk, dv, c->io[0].p, c->io[1].p, (int64_t)H * dk, c->io[2].p,
                            (int64_t)H * dv, c->io[3].p, c->io[4].p, c->io[9].p, bias_dev, nullptr,
                            c->io[7].p, c->io[8].p, c->io[10].p, c->io[5].p);
   if (rc) return rc;
   CUDA_TRY(cudaEventRecord(c->ev[3], st));  // gradients ready
-  CUDA_TRY(cudaStreamWaitEvent(cp, c->ev[3], 0));
-  CUDA_TRY(cudaMemcpyAsync(dq, c->io[7].p, bq, cudaMemcpyDeviceToHost, cp));
-  CUDA_TRY(cudaMemcpyAsync(dk_out, c->io[8].p, bq, cudaMemcpyDeviceToHost, cp));
-  CUDA_TRY(cudaMemcpyAsync(dv_out, c->io[10].p, bv, cudaMemcpyDeviceToHost, cp));
-  if (dbias && E) CUDA_TRY(cudaMemcpyAsync(dbias, c->io[5].p, E * as, cudaMemcpyDeviceToHost, cp));
-  CUDA_TRY(cudaEventRecord(c->ev[0], cp));
-  CUDA_TRY(cudaStreamWaitEvent(st, c->ev[0], 0));  // drain_errors below synchronises st
+  CUDA_TRY(cudaStreamWaitEvent(dn, c->ev[3], 0));
+  CUDA_TRY(cudaMemcpyAsync(dq, c->io[7].p, bq, cudaMemcpyDeviceToHost, dn));
+  CUDA_TRY(cudaMemcpyAsync(dk_out, c->io[8].p, bq, cudaMemcpyDeviceToHost, dn));
+  CUDA_TRY(cudaMemcpyAsync(dv_out, c->io[10].p, bv, cudaMemcpyDeviceToHost, dn));
+  if (dbias && E) CUDA_TRY(cudaMemcpyAsync(dbias, c->io[5].p, E * as, cudaMemcpyDeviceToHost, dn));
+  CUDA_TRY(cudaEventRecord(c->ev[5], dn));  // gradients read back
+  c->pending = true;
+  if (!sync) return GTE_OK;
+  CUDA_TRY(cudaStreamSynchronize(dn));
+  c->pending = false;
   return drain_errors(c);
+}
+
+int gte_sparse_attn_fwd_bwd_host(gte_ctx* c, const gte_plan* plan, int dtype, int H, int dk, int dv,
+                                 const void* q, const void* k, const void* v, const void* dout,
+                                 const void* bias, void* out, void* dq, void* dk_out, void* dv_out,
+                                 void* dbias) {
+  return fwd_bwd_host_impl(c, plan, dtype, H, dk, dv, q, k, v, dout, bias, out, dq, dk_out, dv_out, dbias, true);
+}
+
+int gte_sparse_attn_fwd_bwd_host_async(gte_ctx* c, const gte_plan* plan, int dtype, int H, int dk, int dv,
+                                       const void* q, const void* k, const void* v, const void* dout,
+                                       const void* bias, void* out, void* dq, void* dk_out, void* dv_out,
+                                       void* dbias) {
+  return fwd_bwd_host_impl(c, plan, dtype, H, dk, dv, q, k, v, dout, bias, out, dq, dk_out, dv_out, dbias, false);
 }
 
 }  // extern "C"

@@ -342,6 +342,14 @@ def test_fwd_bwd_host_matches_device_path(cuda, dtype):
         att.fwd_bwd_host(hq, hk, hv, hdo, hb, *outs, hdb)
     for got, nm in zip(outs + [hdb], ("out", "dq", "dk", "dv", "db")):
         assert np.array_equal(got.double().numpy(), r[nm]), nm
+    # asynchronous steps back to back (uploads of one overlap downloads of the previous)
+    for t in outs + [hdb]:
+        t.zero_()
+    for _ in range(4):
+        att.fwd_bwd_host(hq, hk, hv, hdo, hb, *outs, hdb, sync=False)
+    plan.ctx.sync()
+    for got, nm in zip(outs + [hdb], ("out", "dq", "dk", "dv", "db")):
+        assert np.array_equal(got.double().numpy(), r[nm]), nm
 
 
 @pytest.mark.parametrize("dtype,which", [("f32", 0), ("bf16", 0), ("f32", 1), ("bf16", 2)])
