@@ -119,6 +119,13 @@ struct gte_ctx {
   cudaEvent_t ev[8] = {};               // [0] inputs in, [1] dO in, [2] O ready, [3] grads ready,
                                         // [4] O read back, [5] grads read back, [6] scratch
   bool pending = false;                 // a previous fwd_bwd_host step is still in flight
+  // double-buffered device sets of fwd_bwd_host (inputs + outputs), alternated
+  // per step so one step's uploads and downloads overlap the other's kernels:
+  // [0] q [1] k [2] v [3] out [4] lse [5] dbias [6] bias [7] dq [8] dk [9] dO [10] dv
+  DevBuf hs[2][11];
+  cudaEvent_t k_done[2] = {}, d2h_done[2] = {};
+  bool hs_used[2] = {false, false};
+  int parity = 0;
   int* d_err = nullptr;  // [0] non-finite bits, [1] first empty row
   int* h_err = nullptr;  // pinned mirror
   int64_t launches = 0;
@@ -671,6 +678,11 @@ int gte_ctx_destroy(gte_ctx* c) {
     cudaStreamDestroy(c->copy);
     cudaStreamDestroy(c->down);
     for (auto& e : c->ev) cudaEventDestroy(e);
+    for (int s = 0; s < 2; ++s) {
+      cudaEventDestroy(c->k_done[s]);
+      cudaEventDestroy(c->d2h_done[s]);
+      for (auto& b : c->hs[s]) b.release();
+    }
   }
   for (auto& b : c->io) b.release();
   c->scratch.release();
@@ -1002,52 +1014,59 @@ static int fwd_bwd_host_impl(gte_ctx* c, const gte_plan* plan, int dtype, int H,
     CUDA_TRY(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
     CUDA_TRY(cudaStreamCreateWithFlags(&c->down, cudaStreamNonBlocking));
     for (auto& e : c->ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (int s = 0; s < 2; ++s) {
+      CUDA_TRY(cudaEventCreateWithFlags(&c->k_done[s], cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&c->d2h_done[s], cudaEventDisableTiming));
+    }
   }
-  const bool grow = c->io[0].cap < bq || c->io[2].cap < bv || c->io[4].cap < S * H * as ||
-                    c->io[5].cap < (E + 1) * as || c->io[6].cap < (E + 1) * as;
-  if (grow && c->pending) {  // buffers are about to move: finish the step in flight first
+  const int sidx = c->parity;
+  c->parity ^= 1;
+  DevBuf* B = c->hs[sidx];
+  const bool grow = B[0].cap < bq || B[2].cap < bv || B[4].cap < S * H * as || B[5].cap < (E + 1) * as ||
+                    B[6].cap < (E + 1) * as;
+  if (grow && c->pending) {  // this set's buffers are about to move: finish what is in flight
     CUDA_TRY(cudaStreamSynchronize(c->down));
+    CUDA_TRY(cudaStreamSynchronize(st));
     c->pending = false;
   }
-  for (int i : {0, 1, 7, 8}) CUDA_TRY(c->io[i].ensure(bq));
-  for (int i : {2, 3, 9, 10}) CUDA_TRY(c->io[i].ensure(bv));
-  CUDA_TRY(c->io[4].ensure(S * H * as));
-  CUDA_TRY(c->io[5].ensure((E + 1) * as));
-  CUDA_TRY(c->io[6].ensure((E + 1) * as));
+  for (int i : {0, 1, 7, 8}) CUDA_TRY(B[i].ensure(bq));
+  for (int i : {2, 3, 9, 10}) CUDA_TRY(B[i].ensure(bv));
+  CUDA_TRY(B[4].ensure(S * H * as));
+  CUDA_TRY(B[5].ensure((E + 1) * as));
+  CUDA_TRY(B[6].ensure((E + 1) * as));
   cudaStream_t up = c->copy, dn = c->down;
-  // inputs may be overwritten once the previous step's kernels are done with them
-  CUDA_TRY(cudaEventRecord(c->ev[6], st));
-  CUDA_TRY(cudaStreamWaitEvent(up, c->ev[6], 0));
-  CUDA_TRY(cudaMemcpyAsync(c->io[1].p, k, bq, cudaMemcpyHostToDevice, up));
-  CUDA_TRY(cudaMemcpyAsync(c->io[2].p, v, bv, cudaMemcpyHostToDevice, up));
-  CUDA_TRY(cudaMemcpyAsync(c->io[0].p, q, bq, cudaMemcpyHostToDevice, up));
-  if (bias) CUDA_TRY(cudaMemcpyAsync(c->io[6].p, bias, E * as, cudaMemcpyHostToDevice, up));
+  const bool used = c->hs_used[sidx] && !grow;
+  c->hs_used[sidx] = true;
+  // uploads into this set wait for the kernels of the step that last used it
+  if (used) CUDA_TRY(cudaStreamWaitEvent(up, c->k_done[sidx], 0));
+  CUDA_TRY(cudaMemcpyAsync(B[1].p, k, bq, cudaMemcpyHostToDevice, up));
+  CUDA_TRY(cudaMemcpyAsync(B[2].p, v, bv, cudaMemcpyHostToDevice, up));
+  CUDA_TRY(cudaMemcpyAsync(B[0].p, q, bq, cudaMemcpyHostToDevice, up));
+  if (bias) CUDA_TRY(cudaMemcpyAsync(B[6].p, bias, E * as, cudaMemcpyHostToDevice, up));
   CUDA_TRY(cudaEventRecord(c->ev[0], up));  // forward inputs resident
-  CUDA_TRY(cudaMemcpyAsync(c->io[9].p, dout, bv, cudaMemcpyHostToDevice, up));
+  CUDA_TRY(cudaMemcpyAsync(B[9].p, dout, bv, cudaMemcpyHostToDevice, up));
   CUDA_TRY(cudaEventRecord(c->ev[1], up));  // dO resident
-  const void* bias_dev = bias ? c->io[6].p : nullptr;
+  const void* bias_dev = bias ? B[6].p : nullptr;
   CUDA_TRY(cudaStreamWaitEvent(st, c->ev[0], 0));
-  if (c->pending) CUDA_TRY(cudaStreamWaitEvent(st, c->ev[4], 0));  // previous O read back
-  rc = gte_sparse_attn_fwd(c, plan, dtype, H, dk, dv, c->io[0].p, c->io[1].p, (int64_t)H * dk, c->io[2].p,
-                           (int64_t)H * dv, bias_dev, nullptr, c->io[3].p, c->io[4].p, 0);
+  // outputs of this set are free once their previous download finished
+  if (used) CUDA_TRY(cudaStreamWaitEvent(st, c->d2h_done[sidx], 0));
+  rc = gte_sparse_attn_fwd(c, plan, dtype, H, dk, dv, B[0].p, B[1].p, (int64_t)H * dk, B[2].p, (int64_t)H * dv,
+                           bias_dev, nullptr, B[3].p, B[4].p, 0);
   if (rc) return rc;
   CUDA_TRY(cudaEventRecord(c->ev[2], st));  // O ready
   CUDA_TRY(cudaStreamWaitEvent(dn, c->ev[2], 0));
-  CUDA_TRY(cudaMemcpyAsync(out, c->io[3].p, bv, cudaMemcpyDeviceToHost, dn));
-  CUDA_TRY(cudaEventRecord(c->ev[4], dn));  // O read back
+  CUDA_TRY(cudaMemcpyAsync(out, B[3].p, bv, cudaMemcpyDeviceToHost, dn));
   CUDA_TRY(cudaStreamWaitEvent(st, c->ev[1], 0));
-  if (c->pending) CUDA_TRY(cudaStreamWaitEvent(st, c->ev[5], 0));  // previous gradients read back
-  rc = gte_sparse_attn_bwd(c, plan, dtype, H, dk, dv, c->io[0].p, c->io[1].p, (int64_t)H * dk, c->io[2].p,
-                           (int64_t)H * dv, c->io[3].p, c->io[4].p, c->io[9].p, bias_dev, nullptr,
-                           c->io[7].p, c->io[8].p, c->io[10].p, c->io[5].p);
+  rc = gte_sparse_attn_bwd(c, plan, dtype, H, dk, dv, B[0].p, B[1].p, (int64_t)H * dk, B[2].p, (int64_t)H * dv,
+                           B[3].p, B[4].p, B[9].p, bias_dev, nullptr, B[7].p, B[8].p, B[10].p, B[5].p);
   if (rc) return rc;
-  CUDA_TRY(cudaEventRecord(c->ev[3], st));  // gradients ready
-  CUDA_TRY(cudaStreamWaitEvent(dn, c->ev[3], 0));
-  CUDA_TRY(cudaMemcpyAsync(dq, c->io[7].p, bq, cudaMemcpyDeviceToHost, dn));
-  CUDA_TRY(cudaMemcpyAsync(dk_out, c->io[8].p, bq, cudaMemcpyDeviceToHost, dn));
-  CUDA_TRY(cudaMemcpyAsync(dv_out, c->io[10].p, bv, cudaMemcpyDeviceToHost, dn));
-  if (dbias && E) CUDA_TRY(cudaMemcpyAsync(dbias, c->io[5].p, E * as, cudaMemcpyDeviceToHost, dn));
-  CUDA_TRY(cudaEventRecord(c->ev[5], dn));  // gradients read back
+  CUDA_TRY(cudaEventRecord(c->k_done[sidx], st));  // gradients ready; this set's inputs free
+  CUDA_TRY(cudaStreamWaitEvent(dn, c->k_done[sidx], 0));
+  CUDA_TRY(cudaMemcpyAsync(dq, B[7].p, bq, cudaMemcpyDeviceToHost, dn));
+  CUDA_TRY(cudaMemcpyAsync(dk_out, B[8].p, bq, cudaMemcpyDeviceToHost, dn));
+  CUDA_TRY(cudaMemcpyAsync(dv_out, B[10].p, bv, cudaMemcpyDeviceToHost, dn));
+  if (dbias && E) CUDA_TRY(cudaMemcpyAsync(dbias, B[5].p, E * as, cudaMemcpyDeviceToHost, dn));
+  CUDA_TRY(cudaEventRecord(c->d2h_done[sidx], dn));  // this set's outputs read back
   c->pending = true;
   if (!sync) return GTE_OK;
   CUDA_TRY(cudaStreamSynchronize(dn));
