@@ -55,7 +55,7 @@ constexpr int kHubDegree = 1024;  // longer rows/columns go to the hub kernels
 #define GTE_TILE_MINB 4
 #endif
 #ifndef GTE_TILE_MINB_COLS
-#define GTE_TILE_MINB_COLS 3
+#define GTE_TILE_MINB_COLS 4
 #endif
 constexpr int kTileEpl = GTE_TILE_EPL;  // edges per slot per step
 
