@@ -161,27 +161,84 @@ class HaloNccl:
                                            y.data_ptr(), ro_.ctypes.data, rc.ctypes.data))
 
 
+class TorchDistHalo:
+    """all_to_allv over an existing torch.distributed group (gloo on CPU for
+    the multi-process tests; one rank per process)."""
+
+    def __init__(self, rank: int, world: int, group=None):
+        self.rank, self.world, self.group = rank, world, group
+
+    def exchange(self, sends: dict, recvs: dict, send_counts: dict, recv_counts: dict, row_elems: int):
+        import torch.distributed as dist
+
+        p = self.rank
+        sc = [int(x) for x in send_counts[p]]
+        rc = [int(x) for x in recv_counts[p]]
+        x = sends[p][: sum(sc)].contiguous()
+        y = recvs[p]
+        out = y.new_empty((sum(rc),) + tuple(y.shape[1:]))
+        dist.all_to_all_single(out, x, output_split_sizes=rc, input_split_sizes=sc, group=self.group)
+        if sum(rc):
+            y[: sum(rc)].copy_(out)
+
+
+class DeviceHaloOps:
+    """The device half of HaloAttention: local plans + the sparse attention
+    kernels, row gather and ordered scatter-add (csrc/sp.cu)."""
+
+    def __init__(self, heads: int, dh: int, dtype: str, ctx=None, schedule: bool = True):
+        self.H, self.dh, self.dtype, self.d = heads, dh, dtype, heads * dh
+        self.ctx = ctx or Context.get(0)
+        self.schedule = schedule
+        self.att = {}
+
+    def setup(self, r: RankHalo):
+        plan = DevicePlan.from_host(r.local_ro, r.local_co, self.ctx)
+        if self.schedule:
+            plan.schedule()
+        self.att[r.rank] = DeviceSparseAttention(plan, self.H, self.dh, self.dh, self.dtype)
+
+    def index(self, idx: np.ndarray):
+        import torch
+
+        return torch.tensor(idx.astype(np.int32), device=torch.device("cuda", self.ctx.device))
+
+    def gather(self, ext, idx, n: int):
+        import torch
+
+        buf = torch.empty((max(n, 1), self.d), dtype=ext.dtype, device=ext.device)
+        if n:
+            check(_bind().gte_rows_gather(self.ctx.h, _lib.DTYPES[self.dtype], n, idx.data_ptr(), ext.data_ptr(),
+                                          self.d, self.d, buf.data_ptr()))
+        return buf
+
+    def scatter_add(self, dst, idx, src, n: int):
+        check(_bind().gte_rows_scatter_add(self.ctx.h, _lib.DTYPES[self.dtype], n, idx.data_ptr(), src.data_ptr(),
+                                           self.d, dst.data_ptr(), self.d))
+
+    def attn_fwd(self, rank, q, k, v, b):
+        return self.att[rank].forward(q, k, v, b)
+
+    def attn_bwd(self, rank, q, k, v, o, lse, do, b):
+        return self.att[rank].backward(q, k, v, o, lse, do, b)
+
+
 class HaloAttention:
     """The sparse attention layer over P ranks with a cluster-halo exchange.
     `ranks` are the RankHalo plans this process holds (all P for the loopback,
-    one for NCCL). Shards: own rows [n_own, H*dh] per rank (CUDA tensors)."""
+    one for NCCL / torch.distributed). Shards: own rows [n_own, H*dh] per
+    rank. `ops` supplies the kernels (DeviceHaloOps unless given)."""
 
     def __init__(self, ranks: list[RankHalo], P: int, heads: int, dh: int, dtype: str, exchange, ctx=None,
-                 schedule: bool = True):
+                 schedule: bool = True, ops=None):
         self.ranks, self.P, self.H, self.dh, self.dtype, self.x = ranks, P, heads, dh, dtype, exchange
-        self.ctx = ctx or Context.get(0)
         self.d = heads * dh
-        self.plans, self.att, self.idx = {}, {}, {}
-        import torch
-
+        self.ops = ops or DeviceHaloOps(heads, dh, dtype, ctx, schedule)
+        self.idx = {}
         for r in ranks:
-            plan = DevicePlan.from_host(r.local_ro, r.local_co, self.ctx)
-            if schedule:
-                plan.schedule()
-            self.plans[r.rank] = plan
-            self.att[r.rank] = DeviceSparseAttention(plan, heads, dh, dh, dtype)
+            self.ops.setup(r)
             cat = np.concatenate(r.send_idx) if r.send_idx else np.zeros(0, np.int32)
-            self.idx[r.rank] = torch.tensor(cat.astype(np.int32), device="cuda")
+            self.idx[r.rank] = self.ops.index(cat)
         self._send_counts = {r.rank: [len(s) for s in r.send_idx] for r in ranks}
         self._recv_counts = {r.rank: list(r.recv_counts) for r in ranks}
         if len(ranks) == P:  # loopback: every rank's counts are local
@@ -192,11 +249,9 @@ class HaloAttention:
     def _ext(self, r: RankHalo, own, zero_tail: bool = False):
         """[own | halo] buffer. Tails that no exchange fills (Q, dO) are zeroed:
         the kernels' padding slots may read any row of the local index space."""
-        import torch
-
         if r.n_ext == r.n_own:
             return own.contiguous()
-        t = torch.empty((r.n_ext, self.d), dtype=own.dtype, device=own.device)
+        t = own.new_empty((r.n_ext, self.d))
         t[: r.n_own].copy_(own)
         if zero_tail:
             t[r.n_own:].zero_()
@@ -204,45 +259,31 @@ class HaloAttention:
 
     def _halo_in(self, tensors: dict):
         """Fill the halo tails of ext buffers {rank: ext} with the owners' rows."""
-        import torch
-
-        L = _bind()
-        code = _lib.DTYPES[self.dtype]
         sends, recvs = {}, {}
         for r in self.ranks:
             ext = tensors[r.rank]
-            n = int(self.idx[r.rank].numel())
-            buf = torch.empty((max(n, 1), self.d), dtype=ext.dtype, device=ext.device)
-            if n:
-                check(L.gte_rows_gather(self.ctx.h, code, n, self.idx[r.rank].data_ptr(), ext.data_ptr(), self.d,
-                                        self.d, buf.data_ptr()))
-            sends[r.rank] = buf
+            sends[r.rank] = self.ops.gather(ext, self.idx[r.rank], int(self.idx[r.rank].numel()))
             recvs[r.rank] = ext[r.n_own:]
         self.x.exchange(sends, recvs, self._all_send_counts(), self._all_recv_counts(), self.d)
 
     def _halo_back(self, tensors: dict):
         """Send the halo rows' partial sums to their owners and add them."""
-        import torch
-
-        L = _bind()
-        code = _lib.DTYPES[self.dtype]
         sends, recvs = {}, {}
         for r in self.ranks:
             ext = tensors[r.rank]
             sends[r.rank] = ext[r.n_own:]
             n = int(self.idx[r.rank].numel())
-            recvs[r.rank] = torch.empty((max(n, 1), self.d), dtype=ext.dtype, device=ext.device)
+            recvs[r.rank] = ext.new_empty((max(n, 1), self.d))
         # reverse direction: what rank p received from q, it now sends back to q
         self.x.exchange(sends, recvs, self._all_recv_counts(), self._all_send_counts(), self.d)
         for r in self.ranks:
-            # one launch per source peer, in rank order: rows are unique within
+            # one call per source peer, in rank order: rows are unique within
             # a peer's block (no atomics) and the summation order is fixed
             off = 0
             idx, rv = self.idx[r.rank], recvs[r.rank]
             for n in self._send_counts[r.rank]:
                 if n:
-                    check(L.gte_rows_scatter_add(self.ctx.h, code, n, idx[off:].data_ptr(), rv[off:].data_ptr(),
-                                                 self.d, tensors[r.rank].data_ptr(), self.d))
+                    self.ops.scatter_add(tensors[r.rank], idx[off:off + n], rv[off:off + n], n)
                 off += n
 
     def _all_send_counts(self):
@@ -261,20 +302,18 @@ class HaloAttention:
         for r in self.ranks:
             qx = self._ext(r, q[r.rank], zero_tail=True)
             b = None if bias is None else bias[r.e_lo:r.e_hi]
-            o, lse = self.att[r.rank].forward(qx, kx[r.rank], vx[r.rank], b)
+            o, lse = self.ops.attn_fwd(r.rank, qx, kx[r.rank], vx[r.rank], b)
             self.cache[r.rank] = (qx, kx[r.rank], vx[r.rank], o, lse, b)
             out[r.rank] = o[: r.n_own]
         return out
 
     def backward(self, dout: dict):
         """Returns {rank: (dq_own, dk_own, dv_own, dbias_own_edges)}."""
-        import torch
-
         gq, gk, gv, gb = {}, {}, {}, {}
         for r in self.ranks:
             qx, kx, vx, o, lse, b = self.cache[r.rank]
             dox = self._ext(r, dout[r.rank], zero_tail=True)
-            dq, dk, dv, db = self.att[r.rank].backward(qx, kx, vx, o, lse, dox, b)
+            dq, dk, dv, db = self.ops.attn_bwd(r.rank, qx, kx, vx, o, lse, dox, b)
             gq[r.rank], gk[r.rank], gv[r.rank], gb[r.rank] = dq, dk, dv, db
         self._halo_back(gk)
         self._halo_back(gv)

@@ -87,3 +87,126 @@ def test_exchange_protocol_matches_oracle(orc):
             assert np.abs(x - y).max() < 1e-12
         db -= f
     assert np.abs(db).max() < 1e-12
+
+
+class CpuHaloOps:
+    """Test-local kernels for HaloAttention on CPU tensors: the oracle's per-head
+    attention on each rank's local plan, numpy-equivalent gather / scatter-add
+    (the checker; the product's device ops are tested in test_halo_gpu.py)."""
+
+    def __init__(self, orc, H, dh):
+        self.orc, self.H, self.dh, self.g = orc, H, dh, {}
+
+    def setup(self, r):
+        from oracle import CSR
+
+        self.g[r.rank] = CSR(r.n_ext, r.local_ro, r.local_co)
+
+    def index(self, idx):
+        import torch
+
+        return torch.tensor(idx.astype(np.int64))
+
+    def gather(self, ext, idx, n):
+        return ext[idx] if n else ext.new_zeros((1, ext.shape[1]))
+
+    def scatter_add(self, dst, idx, src, n):
+        dst[idx] += src
+
+    def _heads(self, x, h):
+        return x[:, h * self.dh:(h + 1) * self.dh].numpy()
+
+    def attn_fwd(self, rank, q, k, v, b):
+        import torch
+
+        o = np.zeros(q.shape)
+        for h in range(self.H):
+            o[:, h * self.dh:(h + 1) * self.dh] = self.orc.sparse_fwd(
+                self._heads(q, h), self._heads(k, h), self._heads(v, h), self.g[rank], None if b is None else b.numpy())
+        return torch.tensor(o), None
+
+    def attn_bwd(self, rank, q, k, v, o, lse, do, b):
+        import torch
+
+        dq, dk, dv = (np.zeros(q.shape) for _ in range(3))
+        db = np.zeros(self.g[rank].nnz)
+        for h in range(self.H):
+            sl = slice(h * self.dh, (h + 1) * self.dh)
+            a, c, e, f = self.orc.sparse_bwd(self._heads(q, h), self._heads(k, h), self._heads(v, h), self.g[rank],
+                                             None if b is None else b.numpy(), None, self._heads(do, h))
+            dq[:, sl], dk[:, sl], dv[:, sl] = a, c, e
+            db += f
+        return torch.tensor(dq), torch.tensor(dk), torch.tensor(dv), torch.tensor(db)
+
+
+def _halo_worker(rank, world, port, path):
+    import os
+    import sys
+
+    import torch
+    import torch.distributed as dist
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    sys.path.insert(0, os.path.join(root, "oracle"))
+    sys.path.insert(0, os.path.join(root, "tests"))
+    from oracle import Oracle
+    from test_halo_cpu import CpuHaloOps
+
+    from paper_2407_14106_b200.halo import HaloAttention, TorchDistHalo, build_halo_plan
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    d = np.load(path)
+    plans = build_halo_plan(d["ro"], d["co"], world)
+    r = plans[rank]
+    H, dh = int(d["H"]), int(d["dh"])
+    layer = HaloAttention([r], world, H, dh, "f64", TorchDistHalo(rank, world), ops=CpuHaloOps(Oracle(), H, dh))
+    t = lambda a: torch.tensor(a[r.lo:r.hi])  # noqa: E731
+    out = layer.forward({rank: t(d["q"])}, {rank: t(d["k"])}, {rank: t(d["v"])}, torch.tensor(d["bias"]))
+    gq, gk, gv, gb = layer.backward({rank: t(d["up"])})[rank]
+    np.savez(path + f".rank{rank}.npz", out=out[rank].numpy(), dq=gq.numpy(), dk=gk.numpy(), dv=gv.numpy(),
+             db=gb.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_ranks_halo_protocol_matches_oracle(orc, tmp_path, world):
+    """HaloAttention with one rank per process over gloo (TorchDistHalo
+    all_to_allv), the oracle as the per-rank kernel: assembled outputs and
+    gradients equal the oracle's single-process layer."""
+    import os
+
+    import torch.multiprocessing as mp
+
+    from oracle import CSR
+
+    H, dh, S = 2, 4, 600
+    ro, co = community_graph(S, 7.0, community=40, seed=world, shuffle=True)
+    rng = np.random.default_rng(world)
+    q, k, v, up = (rng.standard_normal((S, H * dh)) for _ in range(4))
+    bias = rng.normal(0, 0.3, co.shape[0])
+    path = str(tmp_path / "halo.npz")
+    np.savez(path, ro=ro, co=co, q=q, k=k, v=v, up=up, bias=bias, H=H, dh=dh)
+    mp.start_processes(_halo_worker, args=(world, 29300 + os.getpid() % 500 + world, path), nprocs=world,
+                       start_method="spawn")
+    plans = build_halo_plan(ro, co, world)
+    g = CSR(S, ro, co)
+    got = {n: np.zeros((S, H * dh)) for n in ("out", "dq", "dk", "dv")}
+    db = np.zeros(co.shape[0])
+    for r in plans:
+        x = np.load(path + f".rank{r.rank}.npz")
+        for n in got:
+            got[n][r.lo:r.hi] = x[n]
+        db[r.e_lo:r.e_hi] = x["db"]
+    dbw = np.zeros(co.shape[0])
+    for h in range(H):
+        sl = slice(h * dh, (h + 1) * dh)
+        assert np.abs(got["out"][:, sl] - orc.sparse_fwd(q[:, sl], k[:, sl], v[:, sl], g, bias)).max() < 1e-12
+        a, b, c, e = orc.sparse_bwd(q[:, sl], k[:, sl], v[:, sl], g, bias, None, up[:, sl])
+        for n, w in (("dq", a), ("dk", b), ("dv", c)):
+            assert np.abs(got[n][:, sl] - w).max() < 1e-12, n
+        dbw += e
+    assert np.abs(db - dbw).max() < 1e-12
