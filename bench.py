@@ -216,11 +216,12 @@ def run_reference_arm(args, rank, world):
     res = cpu_baseline(ro, co, sample_rows=32768, steps=steps, warmup=max(0, min(args.warmup, 1)))
     line = {"metric": METRIC, "value": res["value"], "unit": "nodes/s", "n_gpus": args.gpus, "steps": steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(res.get("step_s", [0.0])),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": "C3 products-shaped S=262144 H=8 dh=8, reorder k=8 + ECR 5*beta_G d_b=16 "
-                                   "(bounded row sample)", "S": 262144, "E": int(co.shape[0]), "heads": H,
-                       "head_dim": DH, "pattern": args.pattern},
+            "config": {"workload": "C3 ogbn-products-shaped community graph (ids shuffled), S=262144, GPH-slim H=8 "
+                                   "dh=8, cluster reorder k=8 + Elastic reformation beta_thre=5*beta_G d_b=16",
+                       "S": 262144, "E": int(co.shape[0]), "heads": H, "head_dim": DH, "pattern": args.pattern,
+                       "sample": "bounded row sample of the same pattern (see cpu_baseline.sample)"},
             "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": res["value"], "unit": "nodes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
