@@ -20,6 +20,10 @@
 
 #include "attn_sparse.cuh"
 
+#ifndef GTE_BF16_W
+#define GTE_BF16_W 0
+#endif
+
 namespace gte_b200 {
 
 // ---------------------------------------------------------------- packed math
@@ -59,6 +63,7 @@ template <> struct Piece<float> {
     upk(lo, acc[0], acc[1]);
     upk(hi, acc[2], acc[3]);
   }
+  __device__ __forceinline__ static void axpy_w(float w, const uint4& x, float (&acc)[4]) { axpy(w, x, acc); }
   __device__ __forceinline__ static float finite_probe(const uint4& x, float chk) {
     chk = __fmaf_rn(__uint_as_float(x.x), 0.f, chk);
     chk = __fmaf_rn(__uint_as_float(x.y), 0.f, chk);
@@ -98,6 +103,24 @@ template <> struct Piece<__nv_bfloat16> {
       const uint64_t r = ffma2(ww, xv, pk(acc[2 * i], acc[2 * i + 1]));
       upk(r, acc[2 * i], acc[2 * i + 1]);
     }
+  }
+  // acc += w * x with w rounded to bf16 (GTE_BF16_W=1): 8 FHFMA.BF16 with
+  // fp32 accumulation on the packed pairs, no unpacking. The weights are
+  // softmax probabilities / score gradients, which flash attention also
+  // rounds to bf16 before its P·V, dS·K, dS·Q products; 1 and 0 (degree-1
+  // rows) stay exact.
+  __device__ __forceinline__ static void axpy_w(float w, const uint4& x, float (&acc)[8]) {
+#if GTE_BF16_W
+    const unsigned short wb = __bfloat16_as_ushort(__float2bfloat16_rn(w));
+    const uint32_t u[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      asm("{.reg .b16 l, h;\n\tmov.b32 {l, h}, %2;\n\t"
+          "fma.rn.f32.bf16 %0, %3, l, %0;\n\tfma.rn.f32.bf16 %1, %3, h, %1;}"
+          : "+f"(acc[2 * i]), "+f"(acc[2 * i + 1]) : "r"(u[i]), "h"(wb));
+#else
+    axpy(w, x, acc);
+#endif
   }
   __device__ __forceinline__ static float finite_probe(const uint4& x, float chk) {
     // a bf16 pair is non-finite iff one of its exponent fields is all ones

@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(kTileThreads, HALO ? 2 : GTE_TILE_MINB) tile_f
       float pr = M::ex(s[u] - m_use);
       l += pr;
       if (WM && u < rem) pr *= __ldg(wm + (int64_t)g.hcl * p.E + gb + k + u);
-      P::axpy(pr, vr[u], acc);
+      P::axpy_w(pr, vr[u], acc);
     }
     m = m_new;
     k += EPL;
@@ -498,7 +498,7 @@ __global__ void __launch_bounds__(kTileThreads, HALO ? 2 : GTE_TILE_MINB) tile_b
       if (WM && u < rem) dw = __fmul_rn(__ldg(wm + (int64_t)g.hcl * p.E + gb + k + u), dw);
       if (u == 0 && single && k == 0) delta = dw;
       const float ds = (u < rem && !single) ? pr * (dw - delta) : 0.f;
-      P::axpy(ds, kr[u], dq);
+      P::axpy_w(ds, kr[u], dq);
       hs[u] = (g.part == 0 && g.head_ok) ? ds : 0.f;  // one contribution per head
     }
     if (DB) {  // dbias_e = sum over heads (parallel.cpp:319)
@@ -631,8 +631,8 @@ __global__ void __launch_bounds__(kTileThreads, HALO ? 2 : GTE_TILE_MINB_COLS) t
         pw = pr * mult;
       }
       const float ds = pr * (dw - ld[u].y);
-      P::axpy(ds, qr[u], gk);
-      P::axpy(pw, dr[u], gv);
+      P::axpy_w(ds, qr[u], gk);
+      P::axpy_w(pw, dr[u], gv);
     }
     k += EPL;
     const bool done = j >= 0 && k >= d;
@@ -714,7 +714,7 @@ __global__ void __launch_bounds__(kTileThreads) hub_fwd_kernel(SparseArgs p) {
       float pr = M::ex(s[u] - m_use);
       l += pr;
       if (WM && ok[u]) pr *= __ldg(wm + (int64_t)g.hcl * p.E + e0 + u * NS);
-      P::axpy(pr, vr[u], acc);
+      P::axpy_w(pr, vr[u], acc);
     }
     m = m_new;
   }
@@ -802,7 +802,7 @@ __global__ void __launch_bounds__(kTileThreads) hub_bwd_rows_kernel(SparseArgs p
       const float pr = M::ex(__fmaf_rn(sc, scale_l, bl[u]) - lse);
       if (WM && ok[u]) dw = __fmul_rn(__ldg(wm + (int64_t)g.hcl * p.E + e0 + u * NS), dw);
       const float ds = ok[u] ? pr * (dw - delta) : 0.f;
-      P::axpy(ds, kr[u], dq);
+      P::axpy_w(ds, kr[u], dq);
       float hsum = (g.part == 0 && g.head_ok) ? ds : 0.f;
 #pragma unroll
       for (int off = LPH; off < LPN; off <<= 1) hsum += __shfl_xor_sync(0xffffffffu, hsum, off);
@@ -884,8 +884,8 @@ __global__ void __launch_bounds__(kTileThreads) hub_bwd_cols_kernel(SparseArgs p
         pw = pr * mult;
       }
       const float ds = pr * (dw - ld[u].y);
-      P::axpy(ds, qr[u], gk);
-      P::axpy(pw, dr[u], gv);
+      P::axpy_w(ds, qr[u], gk);
+      P::axpy_w(pw, dr[u], gv);
     }
   }
 #pragma unroll
