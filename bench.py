@@ -198,7 +198,9 @@ def cached_workload(pattern, info):
     try:
         pf = info["_perm_forward"]
         meta = {k: v for k, v in info.items() if not k.startswith("_")}
-        np.savez(path, ro=ro, co=co, perm=pf, info=np.array(json.dumps(meta)))
+        tmp = f"{path}.{os.getpid()}.npz"  # ranks of one node may race: write aside, rename atomically
+        np.savez(tmp, ro=ro, co=co, perm=pf, info=np.array(json.dumps(meta)))
+        os.replace(tmp, path)
     except OSError:
         pass
     return ro, co

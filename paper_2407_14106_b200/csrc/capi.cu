@@ -1094,6 +1094,7 @@ namespace gte_b200 {
 int set_error(int code, const std::string& msg) { return fail(code, msg); }
 int64_t& ctx_launch_counter(gte_ctx* c) { return c->launches; }
 void* ctx_stream(gte_ctx* c) { return (void*)c->stream; }
+int ctx_device(gte_ctx* c) { return c->device; }
 // grow-only device workspace owned by the context (stream-ordered use only)
 void* ctx_scratch(gte_ctx* c, size_t bytes) { return c->scratch.ensure(bytes) == cudaSuccess ? c->scratch.p : nullptr; }
 

@@ -33,6 +33,7 @@ namespace gte_b200 {
 int set_error(int code, const std::string& msg);
 int64_t& ctx_launch_counter(gte_ctx* c);
 void* ctx_stream(gte_ctx* c);
+int ctx_device(gte_ctx* c);
 }  // namespace gte_b200
 
 using namespace gte_b200;
@@ -414,9 +415,14 @@ int gte_nccl_unique_id(void* id_out) {
 }
 
 int gte_comm_create(gte_ctx* ctx, int nranks, int rank, const void* id_in, gte_comm** out) {
-  (void)ctx;
   if (nranks < 1 || rank < 0 || rank >= nranks) return set_error(GTE_CONFIG, "comm: bad rank / world size");
   NCCL_API_OR_FAIL();
+  // ncclCommInitRank binds the communicator to the calling thread's device:
+  // make that the context's GPU (one rank per GPU)
+  if (ctx) {
+    const cudaError_t e = cudaSetDevice(ctx_device(ctx));
+    if (e != cudaSuccess) return set_error(GTE_CUDA, std::string("CUDA error: ") + cudaGetErrorString(e));
+  }
   ncclUniqueId id;
   memcpy(&id, id_in, sizeof id);
   auto* c = new gte_comm();
