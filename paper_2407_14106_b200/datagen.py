@@ -118,3 +118,19 @@ def community_graph(n: int, arcs_per_node: float, community: int = 256, intra: f
 def products_c3(seed: int = 7):
     """C3: S = 262,144, ~25.26 arcs/node -> E ~ 6.8M incl. loops."""
     return community_graph(262144, 61859140 / 2449029, community=256, intra=0.8, sigma=1.0, seed=seed)
+
+
+def arxiv_c2(seed: int = 11, n: int = 169343, arcs: int = 1166243):
+    """C2 (ogbn-arxiv shape): n = 169,343 nodes with exactly
+    `arcs` distinct non-loop arcs (uniform endpoints, oversampled then cut),
+    plus every self-loop -> E = 1,335,586. Returns (row_off, cols) int64."""
+    rs = np.random.default_rng(seed)
+    keys = np.empty(0, dtype=np.int64)
+    while keys.shape[0] < arcs:
+        m = int(1.1 * (arcs - keys.shape[0])) + 1024
+        s = rs.integers(0, n, m, dtype=np.int64)
+        t = rs.integers(0, n, m, dtype=np.int64)
+        k = s[s != t] * n + t[s != t]
+        keys = np.unique(np.concatenate([keys, k]))
+    keys = rs.permutation(keys)[:arcs]
+    return csr_from_pairs(n, keys // n, keys % n)

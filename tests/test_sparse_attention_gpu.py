@@ -17,7 +17,7 @@ from oracle import CSR
 
 from paper_2407_14106_b200 import attention as A
 from paper_2407_14106_b200._lib import ConfigError, DataError
-from paper_2407_14106_b200.datagen import c1_edges, community_graph, csr_from_pairs
+from paper_2407_14106_b200.datagen import arxiv_c2, c1_edges, community_graph, csr_from_pairs
 
 pytestmark = pytest.mark.gpu
 
@@ -127,6 +127,25 @@ def test_c1_multihead(cuda, orc, c1_graph, dtype):
     want = oracle_multihead(orc, g, r, 8, 8)
     for got, w, nm in zip((r["out"], r["dq"], r["dk"], r["dv"], r["db"]), want, ("out", "dq", "dk", "dv", "dbias")):
         assert_close(got, w, dtype, f"C1 {nm}")
+
+
+@pytest.fixture(scope="module")
+def c2_graph():
+    ro, co = arxiv_c2()
+    return CSR(169343, ro, co)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_c2_arxiv_shape_multihead(cuda, orc, c2_graph, dtype):
+    """C2 (BASELINE configs[1]: ogbn-arxiv shape, 169,343 nodes, E = 1,335,586
+    with loops; GT H = 8, dh = 16) at full size against the fp64 oracle, in the
+    community execution order the bench uses."""
+    g = c2_graph
+    assert g.nnz == 1335586
+    r = run_device(g.row_off, g.cols, 8, 16, dtype, seed=5, order="schedule")
+    want = oracle_multihead(orc, g, r, 8, 16)
+    for got, w, nm in zip((r["out"], r["dq"], r["dk"], r["dv"], r["db"]), want, ("out", "dq", "dk", "dv", "dbias")):
+        assert_close(got, w, dtype, f"C2 {nm}")
 
 
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
