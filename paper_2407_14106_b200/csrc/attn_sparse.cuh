@@ -113,6 +113,11 @@ __device__ __forceinline__ A score_of(const A (&q)[DHT], const A (&k)[DHT], A sc
 // ----------------------------------------------------------------------------
 // forward
 // ----------------------------------------------------------------------------
+// chunks per partial of the backward's two-level sums; on for head chunks
+// up to 32 elements (DHT = 64 already spills: it keeps one running sum)
+constexpr int kSumBlock = 64;
+__host__ __device__ constexpr bool two_level_sums(int dht) { return dht <= 32; }
+
 template <typename T, int DHT, int LPN>
 __global__ void __launch_bounds__(256) sparse_fwd_kernel(SparseArgs p) {
   using A = typename AccOf<T>::type;
@@ -295,8 +300,16 @@ __global__ void __launch_bounds__(256) sparse_bwd_rows_kernel(SparseArgs p) {
 #pragma unroll
       for (int t = 0; t < DHT; ++t) q[t] = d[t] = A(0);
     }
-    for (int e0 = beg; e0 < end; e0 += CHUNK) {
-      const int n = min(CHUNK, end - e0);
+    A tq[DHT];  // two-level sum as in the CSC pass (degree-S hub rows)
+#pragma unroll
+    for (int t = 0; t < DHT; ++t) tq[t] = A(0);
+    for (int b0 = beg; b0 < end; b0 += kSumBlock * CHUNK) {
+    const int b1 = min(end, b0 + kSumBlock * CHUNK);
+    if (two_level_sums(DHT))
+#pragma unroll
+      for (int t = 0; t < DHT; ++t) dq[t] = A(0);
+    for (int e0 = b0; e0 < b1; e0 += CHUNK) {
+      const int n = min(CHUNK, b1 - e0);
       const int my_col = lane < n ? __ldg(p.cols + e0 + lane) : 0;
       const A my_b = (bias && lane < n) ? __ldg(bias + e0 + lane) * A(M::kLogScale) : A(0);
 #pragma unroll
@@ -323,6 +336,13 @@ __global__ void __launch_bounds__(256) sparse_bwd_rows_kernel(SparseArgs p) {
         if (DB && hl == 0 && idx < n) DB[e0 + idx] = ds;
       }
     }
+    if (two_level_sums(DHT))
+#pragma unroll
+      for (int t = 0; t < DHT; ++t) tq[t] += dq[t];
+    }
+    if (two_level_sums(DHT))
+#pragma unroll
+      for (int t = 0; t < DHT; ++t) dq[t] = tq[t];
 #pragma unroll
     for (int off = LPN; off < kWarp; off <<= 1)
 #pragma unroll
@@ -375,8 +395,20 @@ __global__ void __launch_bounds__(256) sparse_bwd_cols_kernel(SparseArgs p) {
 #pragma unroll
       for (int t = 0; t < DHT; ++t) kr[t] = vr[t] = A(0);
     }
-    for (int e0 = beg; e0 < end; e0 += CHUNK) {
-      const int n = min(CHUNK, end - e0);
+    // two-level sum: a fresh partial per block of kSumBlock * CHUNK edges,
+    // added into the total (a degree-S hub column, e.g. a global token's
+    // ~5e5 in-edges, keeps ~(block + blocks) roundings instead of ~S;
+    // columns shorter than one block see the same operations as one level)
+    A tk[DHT], tv[DHT];
+#pragma unroll
+    for (int t = 0; t < DHT; ++t) tk[t] = tv[t] = A(0);
+    for (int b0 = beg; b0 < end; b0 += kSumBlock * CHUNK) {
+    const int b1 = min(end, b0 + kSumBlock * CHUNK);
+    if (two_level_sums(DHT))
+#pragma unroll
+      for (int t = 0; t < DHT; ++t) gk[t] = gv[t] = A(0);
+    for (int e0 = b0; e0 < b1; e0 += CHUNK) {
+      const int n = min(CHUNK, b1 - e0);
       const int my_row = lane < n ? __ldg(p.csc_row + e0 + lane) : 0;
       const int my_eid = lane < n ? __ldg(p.csc_eid + e0 + lane) : 0;
       const A my_b = (bias && lane < n) ? __ldg(bias + my_eid) * A(M::kLogScale) : A(0);
@@ -410,6 +442,19 @@ __global__ void __launch_bounds__(256) sparse_bwd_cols_kernel(SparseArgs p) {
         }
       }
     }
+    if (two_level_sums(DHT))
+#pragma unroll
+      for (int t = 0; t < DHT; ++t) {
+        tk[t] += gk[t];
+        tv[t] += gv[t];
+      }
+    }
+    if (two_level_sums(DHT))
+#pragma unroll
+      for (int t = 0; t < DHT; ++t) {
+        gk[t] = tk[t];
+        gv[t] = tv[t];
+      }
 #pragma unroll
     for (int off = LPN; off < kWarp; off <<= 1)
 #pragma unroll

@@ -134,3 +134,15 @@ def arxiv_c2(seed: int = 11, n: int = 169343, arcs: int = 1166243):
         keys = np.unique(np.concatenate([keys, k]))
     keys = rs.permutation(keys)[:arcs]
     return csr_from_pairs(n, keys // n, keys % n)
+
+
+def malnet_c4(seed: int = 13, n: int = 524288, arcs_per_node: float = 35167 / 15378):
+    """C4 (MalNet shape): n = 524,288 graph nodes at 2.29
+    arcs/node plus one global token (index n) attending to and attended by
+    every node (proj/src/model.cpp:349-357), self-loops added ->
+    E ~ 2.77M. Returns (row_off, cols) int64 over n + 1 rows."""
+    ro, co = community_graph(n, arcs_per_node, community=256, intra=0.8, sigma=1.0, seed=seed)
+    src = np.repeat(np.arange(n, dtype=np.int64), np.diff(ro))
+    nodes = np.arange(n, dtype=np.int64)
+    glob = np.full(n, n, dtype=np.int64)
+    return csr_from_pairs(n + 1, np.concatenate([src, nodes, glob]), np.concatenate([co, glob, nodes]))

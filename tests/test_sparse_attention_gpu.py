@@ -17,7 +17,7 @@ from oracle import CSR
 
 from paper_2407_14106_b200 import attention as A
 from paper_2407_14106_b200._lib import ConfigError, DataError
-from paper_2407_14106_b200.datagen import arxiv_c2, c1_edges, community_graph, csr_from_pairs
+from paper_2407_14106_b200.datagen import arxiv_c2, c1_edges, malnet_c4, community_graph, csr_from_pairs
 
 pytestmark = pytest.mark.gpu
 
@@ -146,6 +146,40 @@ def test_c2_arxiv_shape_multihead(cuda, orc, c2_graph, dtype):
     want = oracle_multihead(orc, g, r, 8, 16)
     for got, w, nm in zip((r["out"], r["dq"], r["dk"], r["dv"], r["db"]), want, ("out", "dq", "dk", "dv", "dbias")):
         assert_close(got, w, dtype, f"C2 {nm}")
+
+
+def test_c4_malnet_shape_global_token(cuda, orc):
+    """C4 (BASELINE configs[3] shape: 524,288 nodes + a global token attending
+    to / attended by every node, E = 2.84M; GPH-large H = 32, dh = 24) at full
+    size in f32: the degree-524,289 row and column go through the hub path.
+    Heads 0, 13 and 31 are checked against the fp64 oracle (the oracle runs
+    ~2.5 s per head); dbias, a sum over all 32 heads, only for finiteness
+    (its head-summed parity is covered at C1/C2 and by the hub tests)."""
+    import torch
+
+    ro, co = malnet_c4()
+    S, E, H, dh = ro.shape[0] - 1, co.shape[0], 32, 24
+    dev = torch.device("cuda:0")
+    g = torch.Generator(device=dev).manual_seed(9)
+    q, k, v, do = (torch.randn((S, H * dh), generator=g, device=dev) for _ in range(4))
+    bias = 0.3 * torch.randn(E, generator=g, device=dev)
+    plan = A.DevicePlan.from_host(ro, co)
+    plan.schedule()
+    att = A.DeviceSparseAttention(plan, H, dh, dh, "f32")
+    out, lse = att.forward(q, k, v, bias, None)
+    dq, dk, dv, db = att.backward(q, k, v, out, lse, do, bias, None)
+    plan.ctx.sync()
+    G = CSR(S, ro, co)
+    b64 = bias.double().cpu().numpy()
+    for h in (0, 13, 31):
+        sl = slice(h * dh, (h + 1) * dh)
+        f = lambda t: t[:, sl].double().cpu().numpy()  # noqa: E731
+        qh, kh, vh, doh = f(q), f(k), f(v), f(do)
+        assert_close(f(out), orc.sparse_fwd(qh, kh, vh, G, b64, None), "f32", f"C4 head {h} out")
+        wq, wk, wv, _ = orc.sparse_bwd(qh, kh, vh, G, b64, None, doh)
+        for got, w, nm in ((dq, wq, "dq"), (dk, wk, "dk"), (dv, wv, "dv")):
+            assert_close(f(got), w, "f32", f"C4 head {h} {nm}")
+    assert torch.isfinite(db[:E]).all()
 
 
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
