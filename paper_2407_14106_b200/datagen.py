@@ -146,3 +146,9 @@ def malnet_c4(seed: int = 13, n: int = 524288, arcs_per_node: float = 35167 / 15
     nodes = np.arange(n, dtype=np.int64)
     glob = np.full(n, n, dtype=np.int64)
     return csr_from_pairs(n + 1, np.concatenate([src, nodes, glob]), np.concatenate([co, glob, nodes]))
+
+
+def papers_c5(seed: int = 17):
+    """C5 (ogbn-papers100M shape): S = 1,048,576 at 14.55
+    arcs/node -> E ~ 16M incl. loops; communities of 256, ids shuffled."""
+    return community_graph(1048576, 14.55, community=256, intra=0.8, sigma=1.0, seed=seed)

@@ -17,7 +17,7 @@ from oracle import CSR
 
 from paper_2407_14106_b200 import attention as A
 from paper_2407_14106_b200._lib import ConfigError, DataError
-from paper_2407_14106_b200.datagen import arxiv_c2, c1_edges, malnet_c4, community_graph, csr_from_pairs
+from paper_2407_14106_b200.datagen import arxiv_c2, c1_edges, malnet_c4, papers_c5, community_graph, csr_from_pairs
 
 pytestmark = pytest.mark.gpu
 
@@ -179,6 +179,44 @@ def test_c4_malnet_shape_global_token(cuda, orc):
         wq, wk, wv, _ = orc.sparse_bwd(qh, kh, vh, G, b64, None, doh)
         for got, w, nm in ((dq, wq, "dq"), (dk, wk, "dk"), (dv, wv, "dv")):
             assert_close(f(got), w, "f32", f"C4 head {h} {nm}")
+    assert torch.isfinite(db[:E]).all()
+
+
+@pytest.fixture(scope="module")
+def c5_graph():
+    return papers_c5()
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_c5_papers_shape_heads(cuda, orc, c5_graph, dtype):
+    """C5 (BASELINE configs[4] shape on one GPU: S = 1,048,576, E ~ 16M,
+    GPH-slim H = 8, dh = 8) at full size through the tile kernels in community
+    order; heads 0 and 5 against the fp64 oracle (~5 s per head)."""
+    import torch
+
+    ro, co = c5_graph
+    S, E, H, dh = ro.shape[0] - 1, co.shape[0], 8, 8
+    dev = torch.device("cuda:0")
+    td = _torch_dtype(dtype)
+    g = torch.Generator(device=dev).manual_seed(21)
+    q, k, v, do = (torch.randn((S, H * dh), generator=g, device=dev).to(td) for _ in range(4))
+    bias = 0.3 * torch.randn(E, generator=g, device=dev)
+    plan = A.DevicePlan.from_host(ro, co)
+    plan.schedule()
+    att = A.DeviceSparseAttention(plan, H, dh, dh, dtype)
+    out, lse = att.forward(q, k, v, bias, None)
+    dq, dk, dv, db = att.backward(q, k, v, out, lse, do, bias, None)
+    plan.ctx.sync()
+    G = CSR(S, ro, co)
+    b64 = bias.double().cpu().numpy()
+    for h in (0, 5):
+        sl = slice(h * dh, (h + 1) * dh)
+        f = lambda t: t[:, sl].double().cpu().numpy()  # noqa: E731
+        qh, kh, vh, doh = f(q), f(k), f(v), f(do)
+        assert_close(f(out), orc.sparse_fwd(qh, kh, vh, G, b64, None), dtype, f"C5 head {h} out")
+        wq, wk, wv, _ = orc.sparse_bwd(qh, kh, vh, G, b64, None, doh)
+        for got, w, nm in ((dq, wq, "dq"), (dk, wk, "dk"), (dv, wv, "dv")):
+            assert_close(f(got), w, dtype, f"C5 head {h} {nm}")
     assert torch.isfinite(db[:E]).all()
 
 
