@@ -182,6 +182,27 @@ def test_c4_malnet_shape_global_token(cuda, orc):
     assert torch.isfinite(db[:E]).all()
 
 
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_c3_bench_pattern_full_size(cuda, orc, dtype):
+    """C3, the bench's own workload (BASELINE configs[2]: products shape,
+    S = 262,144, cluster reorder k = 8 + Elastic layout at 5 beta_G, d_b = 16,
+    E = 6.39M; GPH-slim H = 8, dh = 8) at full size in community order: all
+    heads and the head-summed dbias against the fp64 oracle."""
+    import os
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+
+    ro, co = bench.cached_workload("ecr", {})
+    g = CSR(ro.shape[0] - 1, ro.astype(np.int64), co.astype(np.int64))
+    assert g.n == 262144
+    r = run_device(g.row_off, g.cols, 8, 8, dtype, seed=4, order="schedule")
+    want = oracle_multihead(orc, g, r, 8, 8)
+    for got, w, nm in zip((r["out"], r["dq"], r["dk"], r["dv"], r["db"]), want, ("out", "dq", "dk", "dv", "dbias")):
+        assert_close(got, w, dtype, f"C3 {nm}")
+
+
 @pytest.fixture(scope="module")
 def c5_graph():
     return papers_c5()
