@@ -162,6 +162,7 @@ int gte_pattern_buckets(gte_ctx* ctx, int64_t rows, int64_t nnz, const int32_t* 
 int gte_bias_from_table(gte_ctx* ctx, int64_t nnz, const int32_t* d_buckets, const float* d_table, int64_t n_buckets,
                         float* d_bias) {
   if (n_buckets < 1 || n_buckets > kMaxBuckets) return set_error(GTE_CONFIG, "bias_from_table: bucket count out of range");
+  if (nnz >= INT32_MAX) return set_error(GTE_CONFIG, "bias_from_table: pattern too large");
   if (nnz <= 0) return GTE_OK;
   cudaStream_t st = (cudaStream_t)ctx_stream(ctx);
   const int64_t g = (nnz + 255) / 256;
@@ -175,6 +176,7 @@ int gte_bias_from_table(gte_ctx* ctx, int64_t nnz, const int32_t* d_buckets, con
 int gte_dbias_to_table(gte_ctx* ctx, int64_t nnz, const int32_t* d_buckets, const float* d_dbias, int64_t n_buckets,
                        float* d_table_grad, float* d_workspace /* [296 * n_buckets] */) {
   if (n_buckets < 1 || n_buckets > kMaxBuckets) return set_error(GTE_CONFIG, "dbias_to_table: bucket count out of range");
+  if (nnz >= INT32_MAX) return set_error(GTE_CONFIG, "dbias_to_table: pattern too large");
   cudaStream_t st = (cudaStream_t)ctx_stream(ctx);
   table_partial_kernel<<<kTableGrid, 256, 0, st>>>((int32_t)(nnz > 0 ? nnz : 0), d_buckets, d_dbias,
                                                    (int32_t)n_buckets, d_workspace);
