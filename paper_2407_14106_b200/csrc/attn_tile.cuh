@@ -683,7 +683,11 @@ __global__ void __launch_bounds__(kTileThreads) hub_fwd_kernel(SparseArgs p) {
   float m = M::neg_inf(), l = 0.f, acc[VW];
 #pragma unroll
   for (int t = 0; t < VW; ++t) acc[t] = 0.f;
-  for (int e0 = beg + s0; e0 < end; e0 += NS * EPL) {
+  // warp-uniform trip count (the slots of one warp share shuffles in the
+  // head sums): the warp runs while its first slot has edges; lanes past
+  // the end see only masked (ok == false) edges
+  for (int w0 = beg + (int)(threadIdx.x >> 5) * SLOTS; w0 < end; w0 += NS * EPL) {
+    const int e0 = w0 + g.slot;
     uint4 kr[EPL], vr[EPL];
     float bl[EPL];
     bool ok[EPL];
@@ -782,7 +786,11 @@ __global__ void __launch_bounds__(kTileThreads) hub_bwd_rows_kernel(SparseArgs p
   float dq[VW];
 #pragma unroll
   for (int t = 0; t < VW; ++t) dq[t] = 0.f;
-  for (int e0 = beg + s0; e0 < end; e0 += NS * EPL) {
+  // warp-uniform trip count (the slots of one warp share shuffles in the
+  // head sums): the warp runs while its first slot has edges; lanes past
+  // the end see only masked (ok == false) edges
+  for (int w0 = beg + (int)(threadIdx.x >> 5) * SLOTS; w0 < end; w0 += NS * EPL) {
+    const int e0 = w0 + g.slot;
     uint4 kr[EPL], vr[EPL];
     float bl[EPL];
     bool ok[EPL];
@@ -854,7 +862,11 @@ __global__ void __launch_bounds__(kTileThreads) hub_bwd_cols_kernel(SparseArgs p
   float gk[VW], gv[VW];
 #pragma unroll
   for (int t = 0; t < VW; ++t) gk[t] = gv[t] = 0.f;
-  for (int e0 = beg + s0; e0 < end; e0 += NS * EPL) {
+  // warp-uniform trip count (the slots of one warp share shuffles in the
+  // head sums): the warp runs while its first slot has edges; lanes past
+  // the end see only masked (ok == false) edges
+  for (int w0 = beg + (int)(threadIdx.x >> 5) * SLOTS; w0 < end; w0 += NS * EPL) {
+    const int e0 = w0 + g.slot;
     uint4 qr[EPL], dr[EPL];
     float2 ld[EPL];
     float bl[EPL];

@@ -148,17 +148,24 @@ def test_c2_arxiv_shape_multihead(cuda, orc, c2_graph, dtype):
         assert_close(got, w, dtype, f"C2 {nm}")
 
 
-def test_c4_malnet_shape_global_token(cuda, orc):
+@pytest.fixture(scope="module")
+def c4_graph():
+    return malnet_c4()
+
+
+@pytest.mark.parametrize("H,dh", [(32, 24), (8, 8)])
+def test_c4_malnet_shape_global_token(cuda, orc, c4_graph, H, dh):
     """C4 (BASELINE configs[3] shape: 524,288 nodes + a global token attending
     to / attended by every node, E = 2.84M; GPH-large H = 32, dh = 24) at full
-    size in f32: the degree-524,289 row and column go through the hub path.
-    Heads 0, 13 and 31 are checked against the fp64 oracle (the oracle runs
+    size in f32: the degree-524,289 row and column go through the generic
+    kernels' two-level sums (dh = 24) or the tile path's hub kernels (H = 8,
+    dh = 8, the GPH-slim geometry). Heads 0, H/2 and H-1 are checked against the fp64 oracle (the oracle runs
     ~2.5 s per head); dbias, a sum over all 32 heads, only for finiteness
     (its head-summed parity is covered at C1/C2 and by the hub tests)."""
     import torch
 
-    ro, co = malnet_c4()
-    S, E, H, dh = ro.shape[0] - 1, co.shape[0], 32, 24
+    ro, co = c4_graph
+    S, E = ro.shape[0] - 1, co.shape[0]
     dev = torch.device("cuda:0")
     g = torch.Generator(device=dev).manual_seed(9)
     q, k, v, do = (torch.randn((S, H * dh), generator=g, device=dev) for _ in range(4))
@@ -171,7 +178,7 @@ def test_c4_malnet_shape_global_token(cuda, orc):
     plan.ctx.sync()
     G = CSR(S, ro, co)
     b64 = bias.double().cpu().numpy()
-    for h in (0, 13, 31):
+    for h in (0, H // 2, H - 1):
         sl = slice(h * dh, (h + 1) * dh)
         f = lambda t: t[:, sl].double().cpu().numpy()  # noqa: E731
         qh, kh, vh, doh = f(q), f(k), f(v), f(do)
@@ -272,6 +279,23 @@ def test_hub_rows_and_columns_f32(cuda, orc):
     want = oracle_multihead(orc, g, r, 8, 8)
     for got, w, nm in zip((r["out"], r["dq"], r["dk"], r["dv"], r["db"]), want, ("out", "dq", "dk", "dv", "dbias")):
         assert_close(got, w, "f32", f"hub {nm}")
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("n", [1100, 2048, 1038])
+def test_hub_degree_slot_trip_counts(cuda, orc, dtype, n):
+    """Hub rows / columns whose degree leaves the slots of one warp with
+    different trip counts (degree mod (slots x EPL) odd): the hub kernels keep
+    a warp-uniform loop (their head sums shuffle across the warp's slots)."""
+    s = np.arange(n)
+    src = np.r_[s, s, np.full(n, n)]
+    dst = np.r_[(s + 1) % n, np.full(n, n), s]
+    ro, co = csr_from_pairs(n + 1, src, dst)
+    g = CSR(n + 1, ro, co)
+    r = run_device(ro, co, 8, 8, dtype, seed=8)
+    want = oracle_multihead(orc, g, r, 8, 8)
+    for got, w, nm in zip((r["out"], r["dq"], r["dk"], r["dv"], r["db"]), want, ("out", "dq", "dk", "dv", "dbias")):
+        assert_close(got, w, dtype, f"hub d={n + 1} {nm}")
 
 
 @pytest.mark.parametrize("dtype,wm", [("f32", False), ("bf16", False), ("f32", True)])
