@@ -35,6 +35,8 @@ sys.path.insert(0, ROOT)
 METRIC = "graph-attn fwd+bwd nodes/s at S=256K, 1/2/4/8 B200; % of HBM/TC roofline"
 H, DH = 8, 8
 L2_BYTES = 126 * 2 ** 20
+WORKLOAD = ("C3 ogbn-products-shaped community graph (ids shuffled), S=262144, GPH-slim H=8 dh=8, cluster reorder "
+            "k=8 + Elastic reformation beta_thre=5*beta_G d_b=16")
 
 
 def peaks():
@@ -139,35 +141,83 @@ class ClockSampler:
                 "samples": len(rows)}
 
 
-def cpu_baseline(ro, co, sample_rows=131072, steps=3, warmup=1, threads=None):
-    """The compiled reference (oracle/_ref/ref_cpu_bench) on a bounded sample of
-    the same workload, head-parallel on the host cores."""
+def kernel_sources_sha():
+    """sha256 over the CUDA sources of the library (names + bytes, sorted):
+    ties a committed ncu traffic capture to the kernels it measured."""
+    import hashlib
+
+    d = os.path.join(ROOT, "paper_2407_14106_b200", "csrc")
+    h = hashlib.sha256()
+    for name in sorted(os.listdir(d)):
+        if name.endswith((".cu", ".cuh", ".cpp", ".h")):
+            h.update(name.encode())
+            h.update(open(os.path.join(d, name), "rb").read())
+    return h.hexdigest()[:16]
+
+
+def host_cpu():
+    """CPU model and core counts of this host."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except AttributeError:
+        usable = os.cpu_count() or 1
+    return {"cpu_model": model, "nproc": usable, "cpu_count": os.cpu_count()}
+
+
+def cpu_baseline(ro, co, sample_rows=None, steps=3, warmup=1, threads=None, budget_s=None):
+    """The compiled reference (oracle/_ref/ref_cpu_bench) on the same pattern,
+    all H heads, fwd+bwd, on the host cores: head-parallel, and with more
+    cores than heads each head's rows are cut into chunks (SURVEY.md
+    §8(d4)(ii)). sample_rows=None times the whole sequence. budget_s bounds
+    the run: one probe step sets how many of `steps` fit."""
     exe = os.path.join(ROOT, "oracle", "_ref", "ref_cpu_bench")
-    threads = threads or min(H, os.cpu_count() or 1)
+    hc = host_cpu()
+    threads = threads or max(1, min(64, hc["nproc"]))
+    chunks = max(1, threads // H)
     S = ro.shape[0] - 1
+    rows = S if sample_rows is None else min(sample_rows, S)
     if os.path.exists(exe):
         with tempfile.NamedTemporaryFile(suffix=".bin", delete=False) as f:
             np.array([S, co.shape[0]], dtype=np.int64).tofile(f)
             ro.astype(np.int64).tofile(f)
             co.astype(np.int64).tofile(f)
             path = f.name
+
+        def run(k, w):
+            out = subprocess.run([exe, path, str(H), str(DH), str(threads), str(rows), str(k), str(w), "7",
+                                  str(chunks)], capture_output=True, text=True, check=True, timeout=1800).stdout
+            return json.loads(out.strip().splitlines()[-1])
+
         try:
-            out = subprocess.run([exe, path, str(H), str(DH), str(threads), str(sample_rows), str(steps), str(warmup),
-                                  "7"], capture_output=True, text=True, check=True, timeout=900).stdout
+            if budget_s:
+                probe = run(1, 0)["step_s"][0]
+                steps = max(1, min(steps, int(budget_s / max(probe, 1e-3))))
+                warmup = 0  # the probe step was the warm-up
+            d = run(steps, warmup)
         finally:
             os.unlink(path)
-        d = json.loads(out.strip().splitlines()[-1])
         t = statistics.median(d["step_s"])
-        return {"value": sample_rows / t, "unit": "nodes/s", "cores": threads, "kind": "reference",
-                "sample": f"rows [0,{sample_rows}) of the S={S} pattern ({d['pairs']} pairs), all {H} heads, "
-                          f"fwd+bwd, median of {steps} steps; reference proj/src/attention.cpp compiled -O3",
-                "step_s": d["step_s"]}
+        pairs = int(ro[rows]) if rows < S else int(co.shape[0])
+        return {"value": rows / t, "unit": "nodes/s", "cores": threads, "kind": "reference",
+                "sample": (f"{'all ' + str(S) if rows == S else 'rows [0,' + str(rows) + ') of the ' + str(S)} rows "
+                           f"({pairs} pairs), all {H} heads, fwd+bwd, median of {len(d['step_s'])} steps; reference "
+                           f"proj/src/attention.cpp compiled -O3, {threads} threads = {H} heads x {chunks} row "
+                           f"chunks (chunk dK/dV partials summed inside the step)"),
+                "cpu_model": hc["cpu_model"], "nproc": hc["nproc"], "step_s": d["step_s"]}
     # fallback: the C oracle port, single core
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     from oracle import CSR, Oracle
 
     orc = Oracle()
-    rows = min(sample_rows, 16384)
+    rows = min(rows, 16384)
     ro_s = np.minimum(ro, ro[rows])
     g = CSR(S, ro_s, co[: ro[rows]])
     rng = np.random.default_rng(0)
@@ -178,26 +228,39 @@ def cpu_baseline(ro, co, sample_rows=131072, steps=3, warmup=1, threads=None):
         orc.sparse_bwd(q, k, v, g, None, None, up)
     t = time.perf_counter() - t0
     return {"value": rows / t, "unit": "nodes/s", "cores": 1, "kind": "port",
-            "sample": f"rows [0,{rows}), {H} heads sequential, C oracle port"}
+            "sample": f"rows [0,{rows}), {H} heads sequential, C oracle port",
+            "cpu_model": hc["cpu_model"], "nproc": hc["nproc"]}
+
+
+def _cache_path(pattern):
+    return os.path.join(tempfile.gettempdir(), f"gte_c3_{pattern}_v3.npz")
+
+
+def _read_cache(pattern, info):
+    path = _cache_path(pattern)
+    if not os.path.exists(path):
+        return None
+    try:
+        d = np.load(path, allow_pickle=False)
+        info.update(json.loads(str(d["info"])))
+        info["cached"] = True
+        info["_perm_forward"] = d["perm"]
+        return d["ro"], d["co"]
+    except Exception:
+        return None
 
 
 def cached_workload(pattern, info):
-    """make_workload with a best-effort on-disk cache (same inputs -> same
-    pattern; the cache only saves the ~1 min host reorder on repeat runs)."""
-    path = os.path.join(tempfile.gettempdir(), f"gte_c3_{pattern}_v2.npz")
-    if os.path.exists(path):
-        try:
-            d = np.load(path, allow_pickle=False)
-            info.update(json.loads(str(d["info"])))
-            info["cached"] = True
-            info["_perm_forward"] = d["perm"]
-            return d["ro"], d["co"]
-        except Exception:
-            pass
+    """make_workload with an on-disk cache of this run (same inputs -> same
+    pattern; the cache only saves the host reorder/layout on repeat runs)."""
+    got = _read_cache(pattern, info)
+    if got is not None:
+        return got
     ro, co = make_workload(pattern=pattern, info=info)
     try:
         pf = info["_perm_forward"]
         meta = {k: v for k, v in info.items() if not k.startswith("_")}
+        path = _cache_path(pattern)
         tmp = f"{path}.{os.getpid()}.npz"  # ranks of one node may race: write aside, rename atomically
         np.savez(tmp, ro=ro, co=co, perm=pf, info=np.array(json.dumps(meta)))
         os.replace(tmp, path)
@@ -207,24 +270,33 @@ def cached_workload(pattern, info):
 
 
 def run_reference_arm(args, rank, world):
+    """The reference's own CPU implementation (compiled proj/src, oracle/_ref)
+    timed on the whole S = 262,144 sequence with the same pattern and bias
+    recipe as our arm. The pattern is prepared by a SEPARATE process
+    (`bench.py --prepare`, which runs our reorder/layout builders); this
+    process only reads the cached arrays, so no product library is mapped
+    into the reference arm."""
     if rank != 0:
         return
-    import torch
-
-    torch.cuda.set_device(0)  # pattern preparation only; the timed path is the CPU reference
     info = {}
-    ro, co = cached_workload(args.pattern, info)
+    got = _read_cache(args.pattern, info)
+    if got is None:
+        subprocess.run([sys.executable, os.path.abspath(__file__), "--prepare", "--pattern", args.pattern],
+                       check=True, env={k: v for k, v in os.environ.items()
+                                        if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")})
+        got = _read_cache(args.pattern, info)
+    ro, co = got
     steps = max(1, args.steps)
-    res = cpu_baseline(ro, co, sample_rows=32768, steps=steps, warmup=max(0, min(args.warmup, 1)))
-    line = {"metric": METRIC, "value": res["value"], "unit": "nodes/s", "n_gpus": args.gpus, "steps": steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(res.get("step_s", [0.0])),
+    res = cpu_baseline(ro, co, sample_rows=None, steps=steps, warmup=0, budget_s=150.0)
+    line = {"metric": METRIC, "value": res["value"], "unit": "nodes/s", "n_gpus": args.gpus,
+            "steps": len(res.get("step_s", [])), "warmup": 1,
+            "ms_per_step": 1e3 * statistics.median(res.get("step_s", [0.0])),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": "C3 ogbn-products-shaped community graph (ids shuffled), S=262144, GPH-slim H=8 "
-                                   "dh=8, cluster reorder k=8 + Elastic reformation beta_thre=5*beta_G d_b=16",
-                       "S": 262144, "E": int(co.shape[0]), "heads": H, "head_dim": DH, "pattern": args.pattern,
-                       "sample": "bounded row sample of the same pattern (see cpu_baseline.sample)"},
-            "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "config": {"workload": WORKLOAD, "S": int(ro.shape[0] - 1), "E": int(co.shape[0]), "heads": H,
+                       "head_dim": DH, "pattern": args.pattern, "sample": "the whole sequence (same config)",
+                       "preprocess": {k: v for k, v in info.items() if not k.startswith("_")}},
+            "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model", "nproc")},
             "e2e": {"value": res["value"], "unit": "nodes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -389,11 +461,25 @@ def main():
                     help="N > 1: independent replicas (weak scaling) instead of the sequence-parallel layer")
     ap.add_argument("--pattern", default="ecr", choices=["ecr", "edge"],
                     help="ecr: reorder + Elastic layout (default, the C3 config); edge: reordered graph pattern")
+    ap.add_argument("--prepare", action="store_true", help=argparse.SUPPRESS)  # build + cache the pattern only
     args = ap.parse_args()
 
+    if args.prepare:
+        info = {}
+        ro, co = cached_workload(args.pattern, info)
+        print(json.dumps({"prepared": _cache_path(args.pattern), "S": int(ro.shape[0] - 1), "E": int(co.shape[0])}))
+        return
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # one process per GPU: re-launch this command under torchrun
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={29500 + os.getpid() % 1000}",
+               os.path.abspath(__file__)] + sys.argv[1:]
+        os.execv(sys.executable, cmd)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one rank per GPU")
     if args.impl == "reference":
         return run_reference_arm(args, rank, world)
 
@@ -509,10 +595,15 @@ def main():
     hbm, tc, peak_kind = peaks()
     alg = algorithmic_bytes(S, E, e)
     achieved = alg / (ms * 1e-3) / 1e9
-    traffic = None
+    traffic, traffic_src = None, "no capture"
     prof = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.dtype}.json")
     if os.path.exists(prof):
-        traffic = json.load(open(prof)).get("dram_bytes_per_step")
+        tj = json.load(open(prof))
+        if tj.get("kernel_sources_sha") == kernel_sources_sha():
+            traffic = tj.get("dram_bytes_per_step")
+            traffic_src = f"ncu --set full capture {tj.get('source')} of these kernel sources (sha match)"
+        else:
+            traffic_src = f"stale: capture {tj.get('source')} predates the current kernel sources"
     line = {
         "metric": METRIC, "value": world * S / (ms * 1e-3), "unit": "nodes/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -526,7 +617,7 @@ def main():
                    "schedule": "natural" if args.no_schedule else "community (label propagation)",
                    "l2": "flushed between timed steps (2x126MB write); inputs 8x" + f"{S*H*DH*e/2**20:.0f}MB > L2"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                     "traffic": traffic, "peak_source": peak_kind,
+                     "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_kind,
                      "kernel": "tile_fwd + tile_bwd_rows + tile_bwd_cols (3 launches per step)",
                      "algorithmic_bytes_per_step": alg},
         "kernels_ms": {"fwd": float(np.mean(fwd_ms)), "bwd": float(np.mean(bwd_ms))},
@@ -574,8 +665,8 @@ def main():
                              "parity": "bf16: max-norm 2e-2 / L2 1e-2 vs the fp64 oracle" if alt == "bf16"
                              else "f32: max-norm and L2 <= 1e-5 vs the fp64 oracle"}
     if not args.no_cpu_baseline and world == 1:
-        cb = cpu_baseline(ro, co)
-        line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        cb = cpu_baseline(ro, co, sample_rows=None, steps=2, warmup=0, budget_s=30.0)
+        line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model", "nproc")}
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()

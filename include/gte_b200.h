@@ -3,8 +3,9 @@
  * Plain pointers and sizes, no C++ or torch types. Every entry returns a
  * gte_status; on failure gte_last_error() holds a message whose wording
  * follows the reference exception it replaces, so the C++ drop-in layer
- * (include/gte/, csrc/gte_shim.cpp) can rethrow ConfigError/DataError with the
- * same substrings (reference error taxonomy: proj/include/gte/types.hpp:13-24).
+ * (integration/gte_b200_bridge.cpp, compiled against the reference's own
+ * proj/include/gte headers) can rethrow ConfigError/DataError with the same
+ * substrings (reference error taxonomy: proj/include/gte/types.hpp:13-24).
  *
  * Device-pointer entries are stream-ordered on the context's stream and do not
  * synchronise; data-dependent errors (non-finite Q/K/V, empty rows under

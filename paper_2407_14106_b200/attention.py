@@ -342,6 +342,44 @@ class DeviceSparseAttention:
 
         self.plan.ctx.set_stream(torch.cuda.current_stream().cuda_stream)
 
+    def _check(self, qk, vo, acc):
+        """The C ABI takes one leading dimension for the Q-shaped tensors
+        (q, k, dq, dk) and one for the V-shaped ones (v, out, dout, dv): check
+        that they agree, rows are unit-stride, dtypes match this instance and
+        everything sits on one CUDA device. `acc` are the accumulate-typed
+        tensors (lse, bias, weight_mult, dbias)."""
+        import torch
+
+        want = getattr(torch, _TORCH_DT[self.dtype])
+        acc_t = torch.float64 if self.dtype == "f64" else torch.float32
+        S = self.plan.rows
+        dev = None
+        for group, width, name in ((qk, self.H * self.dk, "q/k"), (vo, self.H * self.dv, "v/out")):
+            ld = None
+            for t in group:
+                if t is None:
+                    continue
+                if t.dtype != want:
+                    raise ConfigError(f"sparse_attention: {name} tensor dtype {t.dtype} != {want}")
+                if t.dim() != 2 or t.shape[0] != S or t.shape[1] != width or t.stride(1) != 1:
+                    raise ConfigError(f"sparse_attention: {name} tensors must be [S, {width}] with unit column stride")
+                if ld is None:
+                    ld = t.stride(0)
+                elif t.stride(0) != ld:
+                    raise ConfigError(f"sparse_attention: {name} tensors must share one row stride")
+                dev = dev or t.device
+                if t.device != dev or t.device.type != "cuda":
+                    raise ConfigError("sparse_attention: all tensors must be on the plan's CUDA device")
+        for t in acc:
+            if t is None:
+                continue
+            if t.dtype != acc_t or not t.is_contiguous():
+                raise ConfigError(f"sparse_attention: lse/bias/weight_mult/dbias must be contiguous {acc_t}")
+            if t.device != dev:
+                raise ConfigError("sparse_attention: all tensors must be on the plan's CUDA device")
+        if dev is not None and dev.index is not None and dev.index != self.plan.ctx.device:
+            raise ConfigError("sparse_attention: tensors are not on the plan's device")
+
     def forward(self, q, k, v, bias=None, weight_mult=None, out=None, lse=None, forbid_empty_rows=False):
         import torch
 
@@ -351,6 +389,7 @@ class DeviceSparseAttention:
             out = torch.empty((S, self.H * self.dv), dtype=v.dtype, device=v.device)
         if lse is None:
             lse = torch.empty((S, self.H), dtype=acc, device=v.device)
+        self._check((q, k), (v, out), (lse, bias, weight_mult))
         self._stream()
         check(_lib.lib().gte_sparse_attn_fwd(
             self.plan.ctx.h, self.plan.h, self.code, self.H, self.dk, self.dv, q.data_ptr(), k.data_ptr(),
@@ -368,6 +407,7 @@ class DeviceSparseAttention:
         dv = torch.empty_like(v) if dv is None else dv
         if dbias is None:
             dbias = torch.empty(max(self.plan.nnz, 1), dtype=acc, device=q.device)
+        self._check((q, k, dq, dk), (v, out, dout, dv), (lse, bias, weight_mult, dbias))
         self._stream()
         check(_lib.lib().gte_sparse_attn_bwd(
             self.plan.ctx.h, self.plan.h, self.code, self.H, self.dk, self.dv, q.data_ptr(), k.data_ptr(),

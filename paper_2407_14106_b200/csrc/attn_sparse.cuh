@@ -72,11 +72,6 @@ struct SparseArgs {
   const int32_t* hubs_c = nullptr;
   int n_tiles = 0, n_hubs = 0, n_tiles_c = 0, n_hubs_c = 0;
   void* lsedelta = nullptr;
-  // halo (attn_tile.cuh, HALO kernels): per tile the staged neighbour rows
-  // and the neighbour-id arrays with halo members encoded as ~slot
-  int halo_cap = 0;
-  const int32_t *halo_off = nullptr, *halo_ids = nullptr, *xcols = nullptr;
-  const int32_t *halo_off_c = nullptr, *halo_ids_c = nullptr, *xrows = nullptr;
 };
 
 struct WarpRange {

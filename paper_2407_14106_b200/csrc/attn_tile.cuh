@@ -32,7 +32,7 @@
 // (forward) or partial sums (backward), merged through shared memory.
 #pragma once
 
-#include "attn_rowslot.cuh"
+#include "attn_piece.cuh"
 
 namespace gte_b200 {
 
@@ -68,11 +68,6 @@ struct TileMeta {
 };
 
 constexpr size_t tile_smem_bytes() { return sizeof(TileMeta) + (size_t)(kTileCap + kTilePad) * 8; }
-// halo bytes per tile: cap rows of two tensors (+ the (lse, delta) row of the
-// CSC pass); kept <= kHaloBudget so two CTAs still fit on an SM
-constexpr int kHaloBudget = 48 * 1024;
-inline size_t halo_bytes(int cap, int rowb, int H) { return (size_t)cap * (2 * (size_t)rowb + 8 * (size_t)H); }
-
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
   const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gmem) : "memory");
@@ -83,50 +78,13 @@ __device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefe
 struct TileSmem {
   int* cols;
   float* bias;
-  char* halo;  // [cap][rowb] A rows, [cap][rowb] B rows, [cap][H] float2 (CSC pass)
 };
 
 __device__ __forceinline__ TileSmem tile_carve(unsigned char* raw) {
   TileSmem s;
   s.cols = reinterpret_cast<int*>(raw + sizeof(TileMeta));
   s.bias = reinterpret_cast<float*>(s.cols + kTileCap + kTilePad);
-  s.halo = reinterpret_cast<char*>(s.bias + kTileCap + kTilePad);
   return s;
-}
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
-}
-
-// Issue the cp.async copies of tile blockIdx.x's halo rows: A and B rows
-// (rowb bytes each, 16-byte pieces) and, when L is given, H float2 per row.
-// Completed by tile_stage's wait + barrier.
-__device__ __forceinline__ int halo_issue(const int32_t* __restrict__ off, const int32_t* __restrict__ ids,
-                                          const char* A, uint32_t ra, const char* B, uint32_t rb, int rowb,
-                                          int cap, char* h, const float2* L, int H) {
-  const int h0 = __ldg(off + blockIdx.x), nh = __ldg(off + blockIdx.x + 1) - h0;
-  const int pieces = rowb / 16;
-  char* hA = h;
-  char* hB = h + (size_t)cap * rowb;
-  for (int x = threadIdx.x; x < nh * pieces; x += kTileThreads) {
-    const int r = x / pieces, c = (x % pieces) * 16;
-    const uint32_t row = (uint32_t)__ldg(ids + h0 + r);
-    cp_async16(hA + r * rowb + c, A + row * ra + c);
-    cp_async16(hB + r * rowb + c, B + row * rb + c);
-  }
-  if (L) {
-    float2* hL = reinterpret_cast<float2*>(hB + (size_t)cap * rowb);
-    for (int x = threadIdx.x; x < nh * H; x += kTileThreads) {
-      const int r = x / H, c = x % H;
-      cp_async8(hL + r * H + c, L + (int64_t)__ldg(ids + h0 + r) * H + c);
-    }
-  }
-  return nh;
 }
 
 // Stage tile `blockIdx.x` of the pass. CSR pass: ptr = row_ptr, idx = cols,
@@ -268,8 +226,8 @@ struct EdgeReduce {
 
 // ---------------------------------------------------------------------------
 // Forward: O, LSE (log2 units).
-template <typename T, int LPH, int LPN, int EPL, bool WM, bool HALO>
-__global__ void __launch_bounds__(kTileThreads, HALO ? 2 : GTE_TILE_MINB) tile_fwd_kernel(SparseArgs p) {
+template <typename T, int LPH, int LPN, int EPL, bool WM>
+__global__ void __launch_bounds__(kTileThreads, GTE_TILE_MINB) tile_fwd_kernel(SparseArgs p) {
   using P = Piece<T>;
   using M = SoftmaxMath<float>;
   constexpr int VW = P::N;
@@ -287,12 +245,8 @@ __global__ void __launch_bounds__(kTileThreads, HALO ? 2 : GTE_TILE_MINB) tile_f
   float* __restrict__ LSE = static_cast<float*>(p.lse);
   const uint32_t rq = (uint32_t)(p.ldq * sizeof(T)), rv = (uint32_t)(p.ldv * sizeof(T));
 
-  const int rowb = p.H * p.dk * (int)sizeof(T);
-  if (HALO) halo_issue(p.halo_off, p.halo_ids, K, rq, Vp, rv, rowb, p.halo_cap, sm.halo, nullptr, 0);
-  const int nrows = tile_stage(mt, sm, p.order, p.tiles, p.row_ptr, HALO ? p.xcols : p.cols, nullptr,
+  const int nrows = tile_stage(mt, sm, p.order, p.tiles, p.row_ptr, p.cols, nullptr,
                                static_cast<const float*>(p.bias));
-  const char* hK = sm.halo;
-  const char* hV = sm.halo + (size_t)p.halo_cap * rowb;
   float chk_q = 0.f, chk_k = 0.f, chk_v = 0.f;
   // own-row finiteness of K and V (attention.cpp:20-22): every non-hub row is
   // exactly one tile's own row (hub rows: hub kernel); Q is probed per row
@@ -334,16 +288,9 @@ __global__ void __launch_bounds__(kTileThreads, HALO ? 2 : GTE_TILE_MINB) tile_f
     for (int u = 0; u < EPL; ++u) {
       const int jj = sm.cols[base + u];
       bl[u] = sm.bias[base + u];
-      if (HALO) {  // halo members (~slot) come from shared memory: generic loads
-        const char* kp = jj >= 0 ? K + ((uint32_t)jj * rq + g.bo) : hK + ((uint32_t)(~jj) * rowb + g.bo);
-        const char* vp = jj >= 0 ? Vp + ((uint32_t)jj * rv + g.bo) : hV + ((uint32_t)(~jj) * rowb + g.bo);
-        kr[u] = *reinterpret_cast<const uint4*>(kp);
-        vr[u] = *reinterpret_cast<const uint4*>(vp);
-      } else {
-        const uint32_t j = (uint32_t)jj;
-        kr[u] = ldg16(K, j * rq + g.bo);
-        vr[u] = ldg16(Vp, j * rv + g.bo);
-      }
+      const uint32_t j = (uint32_t)jj;
+      kr[u] = ldg16(K, j * rq + g.bo);
+      vr[u] = ldg16(Vp, j * rv + g.bo);
     }
     float s[EPL];
 #pragma unroll
@@ -399,8 +346,8 @@ __global__ void __launch_bounds__(kTileThreads, HALO ? 2 : GTE_TILE_MINB) tile_f
 // ---------------------------------------------------------------------------
 // CSR pass of the backward: delta, dQ, dbias (summed over heads). Writes the
 // packed (lse, delta) pair per (row, head) for the CSC pass.
-template <typename T, int LPH, int LPN, int EPL, bool WM, bool HALO>
-__global__ void __launch_bounds__(kTileThreads, HALO ? 2 : GTE_TILE_MINB) tile_bwd_rows_kernel(SparseArgs p) {
+template <typename T, int LPH, int LPN, int EPL, bool WM>
+__global__ void __launch_bounds__(kTileThreads, GTE_TILE_MINB) tile_bwd_rows_kernel(SparseArgs p) {
   using P = Piece<T>;
   using M = SoftmaxMath<float>;
   constexpr int VW = P::N;
@@ -422,12 +369,8 @@ __global__ void __launch_bounds__(kTileThreads, HALO ? 2 : GTE_TILE_MINB) tile_b
   float* __restrict__ DB = static_cast<float*>(p.dbias);
   const uint32_t rq = (uint32_t)(p.ldq * sizeof(T)), rv = (uint32_t)(p.ldv * sizeof(T));
 
-  const int rowb = p.H * p.dk * (int)sizeof(T);
-  if (HALO) halo_issue(p.halo_off, p.halo_ids, K, rq, Vp, rv, rowb, p.halo_cap, sm.halo, nullptr, 0);
-  const int nrows = tile_stage(mt, sm, p.order, p.tiles, p.row_ptr, HALO ? p.xcols : p.cols, nullptr,
+  const int nrows = tile_stage(mt, sm, p.order, p.tiles, p.row_ptr, p.cols, nullptr,
                                static_cast<const float*>(p.bias));
-  const char* hK = sm.halo;
-  const char* hV = sm.halo + (size_t)p.halo_cap * rowb;
   float dummy_a = 0.f, dummy_b = 0.f;
   tile_own_rows<T, LPN, false>(mt, nrows, K, rq, Vp, rv, p.H * p.dk * (int)sizeof(T), dummy_a, dummy_b);
   if (threadIdx.x == 0) mt.next = kTileWarps * SLOTS;
@@ -474,16 +417,9 @@ __global__ void __launch_bounds__(kTileThreads, HALO ? 2 : GTE_TILE_MINB) tile_b
     for (int u = 0; u < EPL; ++u) {
       const int jj = sm.cols[base + u];
       bl[u] = sm.bias[base + u];
-      if (HALO) {
-        const char* kp = jj >= 0 ? K + ((uint32_t)jj * rq + g.bo) : hK + ((uint32_t)(~jj) * rowb + g.bo);
-        const char* vp = jj >= 0 ? Vp + ((uint32_t)jj * rv + g.bo) : hV + ((uint32_t)(~jj) * rowb + g.bo);
-        kr[u] = *reinterpret_cast<const uint4*>(kp);
-        vr[u] = *reinterpret_cast<const uint4*>(vp);
-      } else {
-        const uint32_t j = (uint32_t)jj;
-        kr[u] = ldg16(K, j * rq + g.bo);
-        vr[u] = ldg16(Vp, j * rv + g.bo);
-      }
+      const uint32_t j = (uint32_t)jj;
+      kr[u] = ldg16(K, j * rq + g.bo);
+      vr[u] = ldg16(Vp, j * rv + g.bo);
     }
     const bool single = d == 1;
     // delta = dO_i . O_i is set at row start (row_delta); degree-1 rows take
@@ -536,8 +472,8 @@ __global__ void __launch_bounds__(kTileThreads, HALO ? 2 : GTE_TILE_MINB) tile_b
 
 // ---------------------------------------------------------------------------
 // CSC pass of the backward: dK, dV per column, no atomics.
-template <typename T, int LPH, int LPN, int EPL, bool WM, bool HALO>
-__global__ void __launch_bounds__(kTileThreads, HALO ? 2 : GTE_TILE_MINB_COLS) tile_bwd_cols_kernel(SparseArgs p) {
+template <typename T, int LPH, int LPN, int EPL, bool WM>
+__global__ void __launch_bounds__(kTileThreads, GTE_TILE_MINB_COLS) tile_bwd_cols_kernel(SparseArgs p) {
   using P = Piece<T>;
   using M = SoftmaxMath<float>;
   constexpr int VW = P::N;
@@ -557,13 +493,8 @@ __global__ void __launch_bounds__(kTileThreads, HALO ? 2 : GTE_TILE_MINB_COLS) t
   char* DV = static_cast<char*>(p.dv_out);
   const uint32_t rq = (uint32_t)(p.ldq * sizeof(T)), rv = (uint32_t)(p.ldv * sizeof(T));
 
-  const int rowb = p.H * p.dk * (int)sizeof(T);
-  if (HALO) halo_issue(p.halo_off_c, p.halo_ids_c, Q, rq, DO, rv, rowb, p.halo_cap, sm.halo, LD, p.H);
-  const int nrows = tile_stage(mt, sm, p.order_c, p.tiles_c, p.col_ptr, HALO ? p.xrows : p.csc_row, p.csc_eid,
+  const int nrows = tile_stage(mt, sm, p.order_c, p.tiles_c, p.col_ptr, p.csc_row, p.csc_eid,
                                static_cast<const float*>(p.bias));
-  const char* hQ = sm.halo;
-  const char* hD = sm.halo + (size_t)p.halo_cap * rowb;
-  const float2* hL = reinterpret_cast<const float2*>(sm.halo + 2 * (size_t)p.halo_cap * rowb);
   float dummy_a = 0.f, dummy_b = 0.f;
   tile_own_rows<T, LPN, false>(mt, nrows, Q, rq, DO, rv, p.H * p.dk * (int)sizeof(T), dummy_a, dummy_b);
   if (threadIdx.x == 0) mt.next = kTileWarps * SLOTS;
@@ -603,21 +534,10 @@ __global__ void __launch_bounds__(kTileThreads, HALO ? 2 : GTE_TILE_MINB_COLS) t
     for (int u = 0; u < EPL; ++u) {
       const int ii = sm.cols[base + u];
       bl[u] = sm.bias[base + u];
-      if (HALO) {
-        const bool glob = ii >= 0;
-        const uint32_t sl = (uint32_t)(~ii);
-        const char* qp = glob ? Q + ((uint32_t)ii * rq + g.bo) : hQ + (sl * rowb + g.bo);
-        const char* dp = glob ? DO + ((uint32_t)ii * rv + g.bo) : hD + (sl * rowb + g.bo);
-        const float2* lp = glob ? LD + (int64_t)ii * p.H + g.hcl : hL + sl * p.H + g.hcl;
-        qr[u] = *reinterpret_cast<const uint4*>(qp);
-        dr[u] = *reinterpret_cast<const uint4*>(dp);
-        ld[u] = *lp;
-      } else {
-        const uint32_t i = (uint32_t)ii;
-        qr[u] = ldg16(Q, i * rq + g.bo);
-        dr[u] = ldg16(DO, i * rv + g.bo);
-        ld[u] = __ldg(LD + (int64_t)i * p.H + g.hcl);
-      }
+      const uint32_t i = (uint32_t)ii;
+      qr[u] = ldg16(Q, i * rq + g.bo);
+      dr[u] = ldg16(DO, i * rv + g.bo);
+      ld[u] = __ldg(LD + (int64_t)i * p.H + g.hcl);
     }
 #pragma unroll
     for (int u = 0; u < EPL; ++u) {

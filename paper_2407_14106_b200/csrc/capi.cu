@@ -13,10 +13,7 @@
 #include <cub/cub.cuh>
 
 #include "../../include/gte_b200.h"
-#include "fast_launch.cuh"
 #include "tile_launch.cuh"
-#include "wide_launch.cuh"
-#include "prefetch.cuh"
 
 using namespace gte_b200;
 
@@ -100,6 +97,7 @@ __global__ void check_csr_kernel(const int32_t* __restrict__ row_ptr, const int3
     if (cols[i] < 0 || cols[i] >= rows) atomicOr(bad, 1);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += (int64_t)gridDim.x * blockDim.x)
     if (row_ptr[i + 1] < row_ptr[i]) atomicOr(bad, 2);
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (row_ptr[0] != 0 || row_ptr[rows] != nnz)) atomicOr(bad, 2);
 }
 
 unsigned grid_for(int64_t n, int block = 256) {
@@ -150,13 +148,6 @@ struct gte_plan {
   int n_tiles = 0, n_hubs = 0, n_tiles_c = 0, n_hubs_c = 0;
   bool scheduled = false;
   int64_t communities = 0;
-  // halo of the tile kernels (build_halo): per tile the most-referenced
-  // neighbour rows (staged in shared memory once per tile) and the staged
-  // neighbour ids with halo members encoded as ~slot, per pass
-  int halo_cap = 0;          // rows per tile the halo was built for (0: none)
-  int32_t* halo = nullptr;   // one allocation: off, ids, off_c, ids_c, xcols, xrows
-  const int32_t *halo_off = nullptr, *halo_ids = nullptr, *halo_off_c = nullptr, *halo_ids_c = nullptr;
-  const int32_t *xcols = nullptr, *xrows = nullptr;
 };
 
 namespace {
@@ -201,7 +192,21 @@ int build_plan_device(gte_ctx* c, gte_plan* p) {
   CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(int32_t) * (rows + 2), st));
   CUDA_TRY(cudaMemsetAsync(scratch, 0, sizeof(int32_t) * 4, st));
 
+  // validate before any kernel indexes with the pattern: an out-of-range
+  // column or a non-monotone offset must come back as ConfigError, not as a
+  // scatter out of bounds (sticky context error)
   check_csr_kernel<<<grid_for(nnz > rows ? nnz : rows), 256, 0, st>>>(p->row_ptr, p->cols, rows, nnz, scratch);
+  {
+    int32_t bad = 0;
+    CUDA_TRY(cudaMemcpyAsync(&bad, scratch, sizeof bad, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (bad) {
+      for (void* x : {(void*)row_of_edge, (void*)iota, (void*)sorted_cols, (void*)counts, (void*)scratch})
+        cudaFreeAsync(x, st);
+      if (bad & 1) return fail(GTE_CONFIG, "sparse_attention: pattern column out of range");
+      return fail(GTE_CONFIG, "sparse_attention: pattern row offsets not monotone");
+    }
+  }
   if (rows > 0) expand_rows_kernel<<<(unsigned)((rows * 32 + 255) / 256), 256, 0, st>>>(p->row_ptr, rows, row_of_edge);
   iota_kernel<<<grid_for(nnz), 256, 0, st>>>(iota, nnz);
   count_cols_kernel<<<grid_for(nnz), 256, 0, st>>>(p->cols, nnz, counts);
@@ -236,8 +241,6 @@ int build_plan_device(gte_ctx* c, gte_plan* p) {
   cudaFreeAsync(sorted_cols, st);
   cudaFreeAsync(counts, st);
   cudaFreeAsync(scratch, st);
-  if (h[0] & 1) return fail(GTE_CONFIG, "sparse_attention: pattern column out of range");
-  if (h[0] & 2) return fail(GTE_CONFIG, "sparse_attention: pattern row offsets not monotone");
   p->n_unref = h[1];
   p->max_col_deg = rows > 0 ? h[2] : 0;
   p->max_row_deg = rows > 0 ? h[3] : 0;
@@ -309,108 +312,10 @@ int build_exec(gte_plan* p, const int64_t* order) {
   p->order_c = where[1][0];
   p->tiles_c = where[1][1];
   p->hubs_c = where[1][2];
-  cudaFree(p->halo);
-  p->halo = nullptr;
-  p->halo_cap = 0;
   p->n_tiles = (int)ps[0].tiles.size() - 1;
   p->n_hubs = (int)ps[0].hubs.size();
   p->n_tiles_c = (int)ps[1].tiles.size() - 1;
   p->n_hubs_c = (int)ps[1].hubs.size();
-  return GTE_OK;
-}
-
-// Halo of the tile kernels: for every tile of both passes, the (at most
-// `cap`) neighbour rows its edges reference most often (>= 2 references, ties
-// to the smaller id), listed per tile; the staged neighbour-id arrays of both
-// passes with halo members replaced by ~slot (negative). An execution aid
-// only: the kernels read the same K/V (Q/dO/LSE) values from shared memory
-// instead of L2, so outputs are bit-identical with or without it.
-int build_halo(gte_plan* p, int cap) {
-  const int64_t n = p->rows, m = p->nnz;
-  cudaStream_t st = p->ctx->stream;
-  std::vector<int32_t> rp(n + 1), cp(n + 1), ci(m > 0 ? m : 1), cr(m > 0 ? m : 1);
-  std::vector<int32_t> order(n > 0 ? n : 1), tiles(p->n_tiles + 1), order_c(n > 0 ? n : 1), tiles_c(p->n_tiles_c + 1);
-  CUDA_TRY(cudaMemcpyAsync(rp.data(), p->row_ptr, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaMemcpyAsync(cp.data(), p->col_ptr, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost, st));
-  if (m) {
-    CUDA_TRY(cudaMemcpyAsync(ci.data(), p->cols, sizeof(int32_t) * m, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaMemcpyAsync(cr.data(), p->csc_row, sizeof(int32_t) * m, cudaMemcpyDeviceToHost, st));
-  }
-  CUDA_TRY(cudaMemcpyAsync(tiles.data(), p->tiles, sizeof(int32_t) * (p->n_tiles + 1), cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaMemcpyAsync(tiles_c.data(), p->tiles_c, sizeof(int32_t) * (p->n_tiles_c + 1), cudaMemcpyDeviceToHost, st));
-  if (p->n_tiles > 0 && tiles[p->n_tiles] > 0)
-    CUDA_TRY(cudaMemcpyAsync(order.data(), p->order, sizeof(int32_t) * tiles[p->n_tiles], cudaMemcpyDeviceToHost, st));
-  if (p->n_tiles_c > 0 && tiles_c[p->n_tiles_c] > 0)
-    CUDA_TRY(cudaMemcpyAsync(order_c.data(), p->order_c, sizeof(int32_t) * tiles_c[p->n_tiles_c], cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaStreamSynchronize(st));
-  struct Out {
-    std::vector<int32_t> off, ids, x;
-  } out[2];
-  std::vector<int32_t> cnt(n > 0 ? n : 1, 0), slot(n > 0 ? n : 1, -1);
-  for (int pass = 0; pass < 2; ++pass) {
-    const std::vector<int32_t>& ptr = pass == 0 ? rp : cp;
-    const std::vector<int32_t>& nb = pass == 0 ? ci : cr;
-    const std::vector<int32_t>& ord = pass == 0 ? order : order_c;
-    const std::vector<int32_t>& tl = pass == 0 ? tiles : tiles_c;
-    const int nt = pass == 0 ? p->n_tiles : p->n_tiles_c;
-    Out& O = out[pass];
-    O.x.assign(nb.begin(), nb.begin() + (m > 0 ? m : 1));
-    O.off.push_back(0);
-    std::vector<int32_t> seen;
-    for (int t = 0; t < nt; ++t) {
-      seen.clear();
-      for (int x = tl[t]; x < tl[t + 1]; ++x) {
-        const int32_t r = ord[x];
-        for (int32_t e = ptr[r]; e < ptr[r + 1]; ++e) {
-          const int32_t j = nb[e];
-          if (cnt[j]++ == 0) seen.push_back(j);
-        }
-      }
-      std::vector<int32_t> cand;
-      for (int32_t j : seen)
-        if (cnt[j] >= 2) cand.push_back(j);
-      const size_t k = std::min<size_t>(cand.size(), (size_t)cap);
-      std::partial_sort(cand.begin(), cand.begin() + k, cand.end(), [&](int32_t a, int32_t b) {
-        return cnt[a] != cnt[b] ? cnt[a] > cnt[b] : a < b;
-      });
-      for (size_t s2 = 0; s2 < k; ++s2) {
-        slot[cand[s2]] = (int32_t)s2;
-        O.ids.push_back(cand[s2]);
-      }
-      O.off.push_back((int32_t)O.ids.size());
-      for (int x = tl[t]; x < tl[t + 1]; ++x) {
-        const int32_t r = ord[x];
-        for (int32_t e = ptr[r]; e < ptr[r + 1]; ++e)
-          if (slot[nb[e]] >= 0) O.x[e] = ~slot[nb[e]];
-      }
-      for (size_t s2 = 0; s2 < k; ++s2) slot[cand[s2]] = -1;
-      for (int32_t j : seen) cnt[j] = 0;
-    }
-  }
-  size_t total = 0;
-  for (auto& O : out) total += O.off.size() + O.ids.size() + O.x.size();
-  cudaFree(p->halo);
-  p->halo = nullptr;
-  CUDA_TRY(cudaMalloc(&p->halo, sizeof(int32_t) * (total + 1)));
-  int32_t* cur = p->halo;
-  const int32_t* where[2][3];
-  for (int pass = 0; pass < 2; ++pass) {
-    std::vector<int32_t>* v[3] = {&out[pass].off, &out[pass].ids, &out[pass].x};
-    for (int a = 0; a < 3; ++a) {
-      where[pass][a] = cur;
-      if (!v[a]->empty())
-        CUDA_TRY(cudaMemcpyAsync(cur, v[a]->data(), sizeof(int32_t) * v[a]->size(), cudaMemcpyHostToDevice, st));
-      cur += v[a]->size();
-    }
-  }
-  CUDA_TRY(cudaStreamSynchronize(st));
-  p->halo_off = where[0][0];
-  p->halo_ids = where[0][1];
-  p->xcols = where[0][2];
-  p->halo_off_c = where[1][0];
-  p->halo_ids_c = where[1][1];
-  p->xrows = where[1][2];
-  p->halo_cap = cap;
   return GTE_OK;
 }
 
@@ -423,7 +328,6 @@ void free_plan(gte_plan* p) {
   cudaFree(p->csc_eid);
   cudaFree(p->unref);
   cudaFree(p->exec);
-  cudaFree(p->halo);
   delete p;
 }
 
@@ -436,13 +340,11 @@ int pick_lpn(int H) {
   return l;
 }
 
-// Fast (memory-level-parallel) family: f32/bf16, dk == dv, head chunk a
+// Tile family (attn_tile.cuh): f32/bf16, dk == dv, head chunk a
 // power-of-two number of 16-byte pieces, all heads of a neighbour within one
 // warp, 16-byte aligned rows. Returns lanes-per-head, or 0 if not eligible.
 int fast_lph(int dtype, int64_t S, int H, int dk, int dv, int64_t ldq, int64_t ldv,
              std::initializer_list<const void*> ptrs) {
-  static const bool disabled = getenv("GTE_DISABLE_FAST") != nullptr;
-  if (disabled) return 0;
   // 32-bit gather offsets inside the kernels
   if ((S + 1) * (ldq > ldv ? ldq : ldv) * (int64_t)elem_size(dtype) >= (int64_t(1) << 32)) return 0;
   if (dtype != GTE_F32 && dtype != GTE_BF16) return 0;
@@ -459,145 +361,18 @@ int fast_lph(int dtype, int64_t S, int H, int dk, int dv, int64_t ldq, int64_t l
   return lph;
 }
 
-// Halo staging of the tile kernels (opt-in, GTE_HALO=1; measured slower on
-// B200 — generic loads + selects add ~25% instructions and the halo halves
-// occupancy, profiles/r1c/ab_variants.txt): cap rows per tile
-// so that the halo of the CSC pass (Q, dO rows + (lse, delta)) fits
-// kHaloBudget. Built lazily per plan and row width (a per-pattern cache,
-// like the CSC view).
-bool halo_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("GTE_HALO");
-    return e && e[0] == '1';
-  }();
-  return on;
-}
-
-int halo_cap_for(int dtype, int H, int dk) {
-  static const int budget = [] {
-    const char* e = getenv("GTE_HALO_BUDGET");  // bytes per CTA (A/B experiments)
-    return e ? atoi(e) : kHaloBudget;
-  }();
-  const int rowb = H * dk * (int)elem_size(dtype);
-  int cap = budget / (2 * rowb + 8 * H);
-  return cap > 192 ? 192 : cap;
-}
-
-char fast_schedule();
-
-int use_halo(const gte_plan* plan, SparseArgs& a, int dtype, int H, int dk) {
-  if (!halo_enabled() || fast_schedule() != 't') return GTE_OK;
-  const int cap = halo_cap_for(dtype, H, dk);
-  if (cap < 16) return GTE_OK;
-  gte_plan* p = const_cast<gte_plan*>(plan);
-  if (p->halo_cap != cap) {
-    int rc = build_halo(p, cap);
-    if (rc) return rc;
-  }
-  a.halo_cap = p->halo_cap;
-  a.halo_off = p->halo_off;
-  a.halo_ids = p->halo_ids;
-  a.xcols = p->xcols;
-  a.halo_off_c = p->halo_off_c;
-  a.halo_ids_c = p->halo_ids_c;
-  a.xrows = p->xrows;
-  return GTE_OK;
-}
-
-bool prefetch_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("GTE_L2_PREFETCH");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
-
 }  // namespace
-// (gte_ctx is defined below; forward helper)
-static cudaError_t l2_prefetch_impl(cudaStream_t st, int64_t* launches, std::initializer_list<const void*> ptrs,
-                                    std::initializer_list<size_t> bytes) {
-  PrefetchArgs pa{};
-  int n = 0;
-  auto b = bytes.begin();
-  for (const void* p : ptrs) {
-    pa.ptr[n] = static_cast<const char*>(p);
-    pa.bytes[n] = *b++;
-    ++n;
-  }
-  pa.n = n;
-  l2_prefetch_kernel<<<148, 32, 0, st>>>(pa);
-  *launches += 1;
-  return cudaGetLastError();
-}
-static cudaError_t l2_prefetch(gte_ctx* c, std::initializer_list<const void*> ptrs, std::initializer_list<size_t> bytes) {
-  return l2_prefetch_impl(c->stream, &c->launches, ptrs, bytes);
-}
 namespace {
 
-// Kernel schedule for the fast family: 't' tile (default, attn_tile.cuh),
-// 's' row-slot, 'w' warp-per-row (attn_rowslot.cuh / attn_fast.cuh); GTE_SCHED.
-char fast_schedule() {
-  static const char v = [] {
-    const char* e = getenv("GTE_SCHED");
-    return (e && (e[0] == 's' || e[0] == 'w' || e[0] == 'W')) ? e[0] : 't';
-  }();
-  return v;
-}
-
-// Padded tile kernels (attn_wide.cuh; opt-in with GTE_WIDE=16|32, the default
-// is the unpadded attn_tile.cuh family): dense rows (ldq == ldv ==
-// H*dk), head chunk of 16 (bf16), 32 or 64 bytes. Lane pieces of 16 bytes
-// (default) or 32 bytes (GTE_WIDE=32). Returns the piece size in bytes and
-// sets *lpn (lanes per row), or 0 if not eligible.
-int wide_piece(int dtype, int H, int dk, int64_t ldq, int64_t ldv, std::initializer_list<const void*> ptrs,
-               int* lpn) {
-  static const int pb = [] {
-    const char* e = getenv("GTE_WIDE");
-    if (e && atoi(e) == 32) return 32;
-    if (e && atoi(e) == 16) return 16;
-    return 0;  // default: the unpadded tile kernels (faster on B200, profiles/r1c)
-  }();
-  if (pb == 0) return 0;
-  const int64_t es = (int64_t)elem_size(dtype);
-  const int64_t hb = dk * es, rowb = (int64_t)H * dk * es;
-  if (ldq != (int64_t)H * dk || ldv != ldq) return 0;
-  if (!(hb == 32 || hb == 64 || (hb == 16 && dtype == GTE_BF16))) return 0;
-  if (rowb % pb != 0) return 0;
-  const int64_t l = rowb / pb;
-  if (l != 4 && l != 8 && l != 16 && l != 32) return 0;
-  if (l * pb / 16 > 32 || hb / pb > l) return 0;
-  for (const void* q : ptrs)
-    if (q && (reinterpret_cast<uintptr_t>(q) & (pb - 1))) return 0;
-  *lpn = (int)l;
-  return pb;
-}
-
-struct WideSel {
-  int pb = 0, lpn = 0;
-};
-
-cudaError_t dispatch_fast(int dtype, int which, const SparseArgs& a, int lph, cudaStream_t st, int64_t* launches,
-                          WideSel ws = {}) {
+cudaError_t dispatch_tile(int dtype, int which, const SparseArgs& a, int lph, cudaStream_t st, int64_t* launches) {
   int lpn = 1;
   while (lpn < a.H) lpn <<= 1;
   lpn *= lph;
-  if (fast_schedule() == 't' && ws.pb) {
-    int n = 0;
-    const int hb = a.dk * (int)elem_size(dtype);
-    cudaError_t e = dtype == GTE_F32 ? launch_wide_f32(which, a, hb, ws.pb, ws.lpn, st, &n)
-                                     : launch_wide_bf16(which, a, hb, ws.pb, ws.lpn, st, &n);
-    *launches += n;
-    return e;
-  }
-  if (fast_schedule() == 't') {
-    int n = 0;
-    cudaError_t e = dtype == GTE_F32 ? launch_tile_f32(which, a, lph, lpn, st, &n)
-                                     : launch_tile_bf16(which, a, lph, lpn, st, &n);
-    *launches += n;
-    return e;
-  }
-  *launches += 1;
-  return dtype == GTE_F32 ? launch_fast_f32(which, a, lph, lpn, st) : launch_fast_bf16(which, a, lph, lpn, st);
+  int n = 0;
+  cudaError_t e = dtype == GTE_F32 ? launch_tile_f32(which, a, lph, lpn, st, &n)
+                                   : launch_tile_bf16(which, a, lph, lpn, st, &n);
+  *launches += n;
+  return e;
 }
 
 cudaError_t dispatch(int dtype, int which, const SparseArgs& a, int dht, int lpn, cudaStream_t st) {
@@ -738,9 +513,16 @@ int gte_plan_create_host(gte_ctx* c, int64_t rows, int64_t nnz, const int64_t* r
   if (rows < 0 || nnz < 0) return fail(GTE_CONFIG, "plan: negative size");
   if (rows >= INT_MAX || nnz >= INT_MAX) return fail(GTE_CONFIG, "plan: pattern exceeds int32 device index range");
   if (row_off[0] != 0 || row_off[rows] != nnz) return fail(GTE_CONFIG, "sparse_attention: malformed pattern offsets");
+  // host-side validation before narrowing to the int32 device indices: a
+  // column >= 2^31 must not wrap into a valid id
   std::vector<int32_t> ro(rows + 1), co(nnz > 0 ? nnz : 1);
+  for (int64_t i = 0; i < rows; ++i)
+    if (row_off[i + 1] < row_off[i]) return fail(GTE_CONFIG, "sparse_attention: pattern row offsets not monotone");
   for (int64_t i = 0; i <= rows; ++i) ro[i] = (int32_t)row_off[i];
-  for (int64_t i = 0; i < nnz; ++i) co[i] = (int32_t)cols[i];
+  for (int64_t i = 0; i < nnz; ++i) {
+    if (cols[i] < 0 || cols[i] >= rows) return fail(GTE_CONFIG, "sparse_attention: pattern column out of range");
+    co[i] = (int32_t)cols[i];
+  }
   auto* p = new gte_plan();
   p->ctx = c;
   p->rows = rows;
@@ -841,18 +623,8 @@ int gte_sparse_attn_fwd(gte_ctx* c, const gte_plan* plan, int dtype, int H, int 
   a.vec_v = dv == dht && (ldv * es) % 16 == 0 && aligned16(v) && aligned16(out);
   if (plan->rows == 0) return GTE_OK;
   const int lph = fast_lph(dtype, plan->rows, H, dk, dv, ldq, ldv, {q, k, v, out});
-  if (lph && prefetch_enabled() && fast_schedule() != 't') {
-    const size_t rows = (size_t)plan->rows;
-    CUDA_TRY(l2_prefetch(c, {k, v}, {rows * ldq * es, rows * ldv * es}));
-  }
   if (lph) {
-    WideSel wl;
-    wl.pb = wide_piece(dtype, H, dk, ldq, ldv, {q, k, v, out}, &wl.lpn);
-    if (!wl.pb) {
-      rc = use_halo(plan, a, dtype, H, dk);
-      if (rc) return rc;
-    }
-    CUDA_TRY(dispatch_fast(dtype, kFwd, a, lph, c->stream, &c->launches, wl));
+    CUDA_TRY(dispatch_tile(dtype, kFwd, a, lph, c->stream, &c->launches));
   } else {
     CUDA_TRY(dispatch(dtype, kFwd, a, dht, lpn, c->stream));
     c->launches += 1;
@@ -898,22 +670,8 @@ int gte_sparse_attn_bwd(gte_ctx* c, const gte_plan* plan, int dtype, int H, int 
   a.vec_v = dv == dht && (ldv * es) % 16 == 0 && aligned16(v) && aligned16(out) && aligned16(dout) && aligned16(dv_out);
   const int lph = fast_lph(dtype, plan->rows, H, dk, dv, ldq, ldv, {q, k, v, out, dout, dq, dk_out, dv_out});
   if (lph) {
-    const size_t rows = (size_t)plan->rows;
-    const bool pf = prefetch_enabled() && fast_schedule() != 't';
-    if (pf) {
-      CUDA_TRY(l2_prefetch(c, {k, v}, {rows * ldq * es, rows * ldv * es}));
-    }
-    WideSel wl;
-    wl.pb = wide_piece(dtype, H, dk, ldq, ldv, {q, k, v, out, dout, dq, dk_out, dv_out}, &wl.lpn);
-    if (!wl.pb) {
-      rc = use_halo(plan, a, dtype, H, dk);
-      if (rc) return rc;
-    }
-    CUDA_TRY(dispatch_fast(dtype, kBwdRows, a, lph, c->stream, &c->launches, wl));
-    if (pf) {
-      CUDA_TRY(l2_prefetch(c, {q, dout}, {rows * ldq * es, rows * ldv * es}));
-    }
-    CUDA_TRY(dispatch_fast(dtype, kBwdCols, a, lph, c->stream, &c->launches, wl));
+    CUDA_TRY(dispatch_tile(dtype, kBwdRows, a, lph, c->stream, &c->launches));
+    CUDA_TRY(dispatch_tile(dtype, kBwdCols, a, lph, c->stream, &c->launches));
   } else {
     CUDA_TRY(dispatch(dtype, kBwdRows, a, dht, lpn, c->stream));
     CUDA_TRY(dispatch(dtype, kBwdCols, a, dht, lpn, c->stream));

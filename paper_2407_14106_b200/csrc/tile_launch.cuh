@@ -30,26 +30,18 @@ cudaError_t tile_go(K kernel, int grid, size_t smem, const SparseArgs& a, cudaSt
   return cudaGetLastError();
 }
 
-template <typename T, int LPH, int LPN, int EPL, bool WM, bool HALO>
-cudaError_t launch_tile_halo(int which, const SparseArgs& a, cudaStream_t st) {
-  const int rowb = a.H * a.dk * (int)sizeof(T);
-  const size_t smem = tile_smem_bytes() + (HALO ? halo_bytes(a.halo_cap, rowb, a.H) : 0);
-  const int nt = which == kBwdCols ? a.n_tiles_c : a.n_tiles;
-  switch (which) {
-    case kFwd: return tile_go(tile_fwd_kernel<T, LPH, LPN, EPL, WM, HALO>, nt, smem, a, st);
-    case kBwdRows: return tile_go(tile_bwd_rows_kernel<T, LPH, LPN, EPL, WM, HALO>, nt, smem, a, st);
-    default: return tile_go(tile_bwd_cols_kernel<T, LPH, LPN, EPL, WM, HALO>, nt, smem, a, st);
-  }
-}
-
 template <typename T, int LPH, int LPN, int EPL, bool WM>
 cudaError_t launch_tile_one(int which, const SparseArgs& a, cudaStream_t st, int* launches) {
   cudaError_t e = cudaSuccess;
   const int nt = which == kBwdCols ? a.n_tiles_c : a.n_tiles;
   const int nh = which == kBwdCols ? a.n_hubs_c : a.n_hubs;
   if (nt > 0) {
-    e = a.halo_cap > 0 ? launch_tile_halo<T, LPH, LPN, EPL, WM, true>(which, a, st)
-                       : launch_tile_halo<T, LPH, LPN, EPL, WM, false>(which, a, st);
+    const size_t smem = tile_smem_bytes();
+    switch (which) {
+      case kFwd: e = tile_go(tile_fwd_kernel<T, LPH, LPN, EPL, WM>, nt, smem, a, st); break;
+      case kBwdRows: e = tile_go(tile_bwd_rows_kernel<T, LPH, LPN, EPL, WM>, nt, smem, a, st); break;
+      default: e = tile_go(tile_bwd_cols_kernel<T, LPH, LPN, EPL, WM>, nt, smem, a, st); break;
+    }
     if (e != cudaSuccess) return e;
     ++*launches;
   }

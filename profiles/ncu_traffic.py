@@ -26,7 +26,11 @@ def main(path, dtype, tag):
             b += float(r[idx[m]]) * SCALE[units[idx[m]]]
         per[name] = per.get(name, 0.0) + b
         total += b
-    out = {"dram_bytes_per_step": total, "per_kernel": per, "source": os.path.basename(path), "round": tag}
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from bench import kernel_sources_sha
+
+    out = {"dram_bytes_per_step": total, "per_kernel": per, "source": os.path.basename(path), "round": tag,
+           "kernel_sources_sha": kernel_sources_sha()}
     dst = os.path.join(os.path.dirname(os.path.abspath(__file__)), f"ncu_traffic_{dtype}.json")
     json.dump(out, open(dst, "w"), indent=1)
     print(json.dumps(out))
