@@ -222,6 +222,21 @@ class Oracle(_Base):
                    C.c_int64(n_cols), C.c_int64(d_b), _ptr(tiles, I64P), C.c_int64(cap), C.byref(nt))
         return tiles[: 2 * nt.value].reshape(-1, 2)
 
+    def pack_subblocks_sparse(self, er, ec, n_rows, n_cols, d_b):
+        """The same greedy over candidate origins (orc_pack_sparse.cpp)."""
+        er, ec = _i64(er), _i64(ec)
+        m = er.shape[0]
+        cap = max(1, (m + d_b * d_b - 1) // (d_b * d_b)) if d_b >= 1 else 1
+        tiles = np.zeros(2 * cap + 2, dtype=np.int64)
+        nt = C.c_int64()
+        self._call("pack_subblocks_sparse", C.c_int64(m), _ptr(er, I64P), _ptr(ec, I64P), C.c_int64(n_rows),
+                   C.c_int64(n_cols), C.c_int64(d_b), _ptr(tiles, I64P), C.c_int64(cap), C.byref(nt))
+        return tiles[: 2 * nt.value].reshape(-1, 2)
+
+    def set_pack_mode(self, mode: int):
+        """orc_build_layout's packer: 0 auto, 1 coverage field, 2 candidate origins."""
+        self.lib.orc_set_pack_mode(C.c_int(mode))
+
     def build_layout(self, k, bnd, cell_nnz, cell_density, g_perm: CSR, strategy, beta_thre, beta_g, d_b):
         L = _OrcLayout()
         gc = g_perm.to_c()

@@ -13,6 +13,12 @@ int orc_fail(int code, const char* fmt, ...);
 
 static inline int64_t i64abs(int64_t x) { return x < 0 ? -x : x; }
 
+/* packer used by orc_build_layout: 0 auto (the field restatement below for
+ * cells up to 2^24 positions, the candidate-origin restatement of
+ * orc_pack_sparse.cpp above), 1 always the field, 2 always candidates */
+static int g_pack_mode = 0;
+void orc_set_pack_mode(int mode) { g_pack_mode = mode; }
+
 /* pack_subblocks: greedy max-cover of not-yet-covered edges with non-overlapping
  * d_b x d_b tiles; ties keep the first (raster-order) origin; stops only if no
  * free origin remains. reformation.cpp:56-109 (prefix field :15-37). */
@@ -159,8 +165,10 @@ int orc_build_layout(int64_t k, const int64_t* bnd, const int64_t* cell_nnz,
       if (cells[cell].n == 0) continue;
       int64_t cap = (cells[cell].n + d_b * d_b - 1) / (d_b * d_b);
       tiles[cell] = (int64_t*)malloc(sizeof(int64_t) * (size_t)(2 * cap + 2));
-      rc = orc_pack_subblocks(cells[cell].n, cells[cell].r, cells[cell].c, bnd[a + 1] - bnd[a],
-                              bnd[b + 1] - bnd[b], d_b, tiles[cell], cap, &ntile[cell]);
+      const int64_t nr = bnd[a + 1] - bnd[a], nc = bnd[b + 1] - bnd[b];
+      const int sparse = g_pack_mode == 2 || (g_pack_mode == 0 && nr * nc > ((int64_t)1 << 24));
+      rc = (sparse ? orc_pack_subblocks_sparse : orc_pack_subblocks)(cells[cell].n, cells[cell].r, cells[cell].c,
+                                                                     nr, nc, d_b, tiles[cell], cap, &ntile[cell]);
       if (rc) break;
       int64_t covered = 0;
       for (int64_t e = 0; e < cells[cell].n; ++e) {

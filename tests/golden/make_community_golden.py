@@ -92,5 +92,50 @@ def main(name):
                       if np.ndim(v) == 0}))
 
 
+def sha(a):
+    import hashlib
+
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()[:32]
+
+
+def c3_layout():
+    """C3 layout from the reference's own C3 permutation (c3.npz): the oracle's
+    grid (asserted equal to the reference's grid in c3.npz), permute_graph and
+    build_layout with the candidate-origin packer (orc_pack_sparse.cpp — the
+    reference's packer cannot run at this size, see the module docstring).
+    Large arrays are pinned by sha256 (FNV-1a in Python is too slow here)."""
+    from oracle import Oracle
+
+    out = os.path.join(HERE, "c3.npz")
+    d = dict(np.load(out))
+    n, seed = int(d["n"]), int(d["seed"])
+    ro, co = community_graph(n, ARCS, community=256, intra=0.8, sigma=1.0, seed=seed, shuffle=True)
+    O = Oracle()
+    g = CSR(n, ro.astype(np.int64), co.astype(np.int64))
+    fwd = d["reorder_fwd"].astype(np.int64)
+    bnd, cn, cd = O.build_cluster_grid(g, fwd, 8)
+    assert np.array_equal(cn, d["grid_nnz"]) and np.array_equal(cd, d["grid_den"]), "oracle grid != reference grid"
+    gp = O.permute_graph(g, fwd)
+    d["gperm_cols_sha"] = np.array(sha(gp.cols))
+    bg = g.nnz / (float(n) * float(n))
+    O.set_pack_mode(2)
+    t0 = time.time()
+    L = O.build_layout(8, bnd, cn, cd, gp, 1, 5 * bg, bg, 16)
+    d["layout_oracle_s"] = np.float64(time.time() - t0)
+    d["L5bg_state"] = L.cell_state
+    d["L5bg_boff"] = L.block_off
+    d["L5bg_blocks"] = L.blocks
+    d["L5bg_dropped"] = np.int64(L.dropped_edges)
+    d["L5bg_pnnz"] = np.int64(L.pattern.nnz)
+    d["L5bg_pcols_sha"] = np.array(sha(L.pattern.cols))
+    d["L5bg_pro_sha"] = np.array(sha(L.pattern.row_off))
+    np.savez_compressed(out, **d)
+    log(f"c3 layout (oracle, candidate packer) in {d['layout_oracle_s']:.1f} s: {int(L.block_off[-1])} sub-blocks, "
+        f"dropped {L.dropped_edges}, pattern nnz {L.pattern.nnz}; wrote {out}")
+
+
 if __name__ == "__main__":
-    main(sys.argv[1])
+    if sys.argv[1] == "c3layout":
+        c3_layout()
+    else:
+        main(sys.argv[1])

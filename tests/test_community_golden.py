@@ -1,0 +1,147 @@
+"""Integer parity of the cluster-aware pipeline on community-structured graphs
+(the C3 recipe) against the COMPILED REFERENCE.
+
+Fixtures (tests/golden/make_community_golden.py, generated here from
+oracle/_ref): comm16k / comm32k / comm64k hold the reference's reorder(k=8,
+seed=1) permutation, k x k grid and Elastic layout (5 beta_G, d_b=16) in full;
+c3.npz holds the reference's permutation of the bench's own S = 262,144 graph
+and the layout built from it by the oracle's candidate-origin packer (the
+reference packer cannot run at C3; the candidate packer is itself pinned to
+the reference below and at 16K/32K/64K).
+
+reorder (host C++) and the oracle run without a GPU; the product's grid,
+permutation and layout builders run on the GPU (marked gpu).
+"""
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+from oracle import CSR
+
+from paper_2407_14106_b200.datagen import community_graph
+
+ARCS = 61859140 / 2449029
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+SIZES = ["comm16k", "comm32k", "comm64k"]
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()[:32]
+
+
+def load(name):
+    path = os.path.join(GOLD, f"{name}.npz")
+    if not os.path.exists(path):
+        pytest.skip(f"{name}.npz not generated")
+    return np.load(path)
+
+
+def graph_of(d):
+    n = int(d["n"])
+    ro, co = community_graph(n, ARCS, community=256, intra=0.8, sigma=1.0, seed=int(d["seed"]), shuffle=True)
+    assert int(co.shape[0]) == int(d["nnz"])
+    return n, ro, co
+
+
+def _G(n, ro, co):
+    from paper_2407_14106_b200.attention import Graph
+
+    return Graph(n, np.asarray(ro, np.int64), np.asarray(co, np.int64))
+
+
+@pytest.mark.parametrize("name", SIZES + ["c3"])
+def test_reorder_matches_reference(name):
+    """Product reorder (csrc/reorder.cpp) == reference reorder, bit for bit."""
+    from paper_2407_14106_b200 import partition as P
+
+    d = load(name)
+    n, ro, co = graph_of(d)
+    p = P.reorder(_G(n, ro, co), 8, 1)
+    assert np.array_equal(p.forward, d["reorder_fwd"].astype(np.int64))
+    assert p.valid()
+
+
+def test_oracle_candidate_packer_matches_reference_layout(orc):
+    """The oracle's candidate-origin packer reproduces the reference's layout
+    at 16K (full arrays), so it can stand in for it at C3."""
+    d = load("comm16k")
+    n, ro, co = graph_of(d)
+    g = CSR(n, ro, co)
+    fwd = d["reorder_fwd"].astype(np.int64)
+    bnd, cn, cd = orc.build_cluster_grid(g, fwd, 8)
+    assert np.array_equal(cn, d["grid_nnz"]) and np.array_equal(cd, d["grid_den"])
+    gp = orc.permute_graph(g, fwd)
+    bg = g.nnz / (float(n) * n)
+    orc.set_pack_mode(2)
+    try:
+        L = orc.build_layout(8, bnd, cn, cd, gp, 1, 5 * bg, bg, 16)
+    finally:
+        orc.set_pack_mode(0)
+    assert np.array_equal(L.cell_state, d["L5bg_state"])
+    assert np.array_equal(L.block_off, d["L5bg_boff"]) and np.array_equal(L.blocks, d["L5bg_blocks"])
+    assert L.dropped_edges == int(d["L5bg_dropped"]) and L.pattern.nnz == int(d["L5bg_pnnz"])
+
+
+def test_candidate_packer_random_vs_field_packer(orc):
+    rng = np.random.default_rng(11)
+    for t in range(80):
+        nr, nc = (int(x) for x in rng.integers(4, 70, 2))
+        db = int(rng.integers(1, min(nr, nc, 9) + 1))
+        m = int(rng.integers(0, nr * nc // 2 + 1)) if t % 4 else int(rng.integers(0, 6))
+        idx = rng.choice(nr * nc, size=m, replace=False)
+        a = orc.pack_subblocks(idx // nc, idx % nc, nr, nc, db)
+        b = orc.pack_subblocks_sparse(idx // nc, idx % nc, nr, nc, db)
+        assert np.array_equal(a, b), (t, nr, nc, db, m)
+
+
+def _product_pipeline(n, ro, co):
+    from paper_2407_14106_b200 import partition as P
+
+    g = _G(n, ro, co)
+    perm = P.reorder(g, 8, 1)
+    grid = P.build_cluster_grid(g, perm, 8)
+    gp = P.permute_graph(g, perm)
+    bg = P.density(g)
+    return perm, grid, gp, P.build_layout(grid, gp, P.ELASTIC, 5 * bg, bg, 16)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", SIZES)
+def test_layout_matches_reference(cuda, name):
+    """Product grid (fp64 densities), permuted graph and Elastic layout
+    (sub-block list, drops, materialised pattern) == the reference's."""
+    from oracle import fnv1a64_fast
+
+    d = load(name)
+    n, ro, co = graph_of(d)
+    perm, grid, gp, L = _product_pipeline(n, ro, co)
+    assert np.array_equal(perm.forward, d["reorder_fwd"].astype(np.int64))
+    assert np.array_equal(grid.cell_nnz, d["grid_nnz"]) and np.array_equal(grid.cell_density, d["grid_den"])
+    assert fnv1a64_fast(gp.col_indices) == str(d["gperm_cols_fnv"])
+    assert np.array_equal(L.cell_state, d["L5bg_state"])
+    assert np.array_equal(L.block_off, d["L5bg_boff"]) and np.array_equal(L.blocks, d["L5bg_blocks"])
+    assert L.dropped_edges == int(d["L5bg_dropped"]) and L.pattern.nnz() == int(d["L5bg_pnnz"])
+    assert fnv1a64_fast(L.pattern.cols) == str(d["L5bg_pcols_fnv"])
+    assert fnv1a64_fast(L.pattern.row_offsets) == str(d["L5bg_pro_fnv"])
+
+
+@pytest.mark.gpu
+def test_c3_bench_pipeline_matches_reference(cuda):
+    """The bench's own C3 graph: product reorder == reference permutation;
+    product grid == reference grid; product layout == the layout the oracle
+    builds from the reference permutation (sub-blocks, drops, pattern)."""
+    d = load("c3")
+    if "L5bg_blocks" not in d:
+        pytest.skip("c3 layout stage not generated")
+    n, ro, co = graph_of(d)
+    perm, grid, gp, L = _product_pipeline(n, ro, co)
+    assert np.array_equal(perm.forward, d["reorder_fwd"].astype(np.int64))
+    assert np.array_equal(grid.cell_nnz, d["grid_nnz"]) and np.array_equal(grid.cell_density, d["grid_den"])
+    assert sha(np.asarray(gp.col_indices, np.int64)) == str(d["gperm_cols_sha"])
+    assert np.array_equal(L.cell_state, d["L5bg_state"])
+    assert np.array_equal(L.block_off, d["L5bg_boff"]) and np.array_equal(L.blocks, d["L5bg_blocks"])
+    assert L.dropped_edges == int(d["L5bg_dropped"]) and L.pattern.nnz() == int(d["L5bg_pnnz"])
+    assert sha(np.asarray(L.pattern.cols, np.int64)) == str(d["L5bg_pcols_sha"])
+    assert sha(np.asarray(L.pattern.row_offsets, np.int64)) == str(d["L5bg_pro_sha"])
