@@ -87,6 +87,7 @@ def make_workload(seed=7, pattern="ecr", info=None):
     info["transferred_cells"] = L.transferred_cells()
     info["subblocks"] = L.subblock_count()
     info["dropped_edges"] = int(L.dropped_edges)
+    info["_blocks"] = L.global_blocks()  # ECR sub-block origins (tensor-pipe tiles)
     return np.asarray(L.pattern.row_offsets), np.asarray(L.pattern.cols)
 
 
@@ -233,7 +234,7 @@ def cpu_baseline(ro, co, sample_rows=None, steps=3, warmup=1, threads=None, budg
 
 
 def _cache_path(pattern):
-    return os.path.join(tempfile.gettempdir(), f"gte_c3_{pattern}_v3.npz")
+    return os.path.join(tempfile.gettempdir(), f"gte_c3_{pattern}_v4.npz")
 
 
 def _read_cache(pattern, info):
@@ -245,6 +246,7 @@ def _read_cache(pattern, info):
         info.update(json.loads(str(d["info"])))
         info["cached"] = True
         info["_perm_forward"] = d["perm"]
+        info["_blocks"] = d["blocks"]
         return d["ro"], d["co"]
     except Exception:
         return None
@@ -262,7 +264,8 @@ def cached_workload(pattern, info):
         meta = {k: v for k, v in info.items() if not k.startswith("_")}
         path = _cache_path(pattern)
         tmp = f"{path}.{os.getpid()}.npz"  # ranks of one node may race: write aside, rename atomically
-        np.savez(tmp, ro=ro, co=co, perm=pf, info=np.array(json.dumps(meta)))
+        np.savez(tmp, ro=ro, co=co, perm=pf, blocks=np.asarray(info.get("_blocks", np.zeros((0, 2), np.int64))),
+                 info=np.array(json.dumps(meta)))
         os.replace(tmp, path)
     except OSError:
         pass
@@ -454,6 +457,9 @@ def main():
     ap.add_argument("--no-alt", action="store_true", help="skip the other-dtype measurement added to the line")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (profiling runs)")
     ap.add_argument("--no-schedule", action="store_true", help="execute rows in natural order (no community schedule)")
+    ap.add_argument("--ecr-tiles", action="store_true",
+                    help="run the ECR sub-blocks as dense tensor-core tiles (csrc/ecr_tile.cuh; measured slower at C3, "
+                         "profiles/r2d)")
     ap.add_argument("--sp", action="store_true", help="run the sequence-parallel layer even at N = 1 (NCCL, 1 rank)")
     ap.add_argument("--sp-mode", default="halo", choices=["halo", "ulysses"],
                     help="N > 1: cluster-halo row exchange (default) or the reference's Ulysses head split")
@@ -513,6 +519,9 @@ def main():
         t0 = time.perf_counter()
         info["communities"] = plan.schedule()
         info["schedule_s"] = time.perf_counter() - t0
+    if args.pattern == "ecr" and args.ecr_tiles:  # ECR sub-blocks as dense tensor-core tiles (bf16)
+        info["ecr_tiles"] = plan.set_blocks(info["_blocks"], 16)
+        info["ecr_tile_pairs"] = info["ecr_tiles"] * 256
     att = A.DeviceSparseAttention(plan, H, DH, DH, args.dtype)
     out = torch.empty_like(v)
     lse = torch.empty((S, H), dtype=torch.float32, device=dev)

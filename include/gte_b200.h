@@ -84,6 +84,22 @@ int gte_community_order(int64_t n, int64_t nnz, const int64_t* row_off, const in
 int gte_plan_schedule(gte_plan* plan, int64_t iters, int64_t* n_communities);
 int gte_plan_set_order(gte_plan* plan, const int64_t* order);
 
+/* ---- Elastic Computation Reformation on the tensor pipe (the
+ * reference's dense sub-blocks, reformation.cpp:111-195, tile spans
+ * :176-189, executed by cluster_sparse_attention :197-204) ----
+ * gte_plan_set_blocks: registers the layout's d_b x d_b sub-blocks as global
+ *   origins [n_blocks][2] = (row0, col0). With d_b == 16 and a bf16 call whose
+ *   head geometry has tile kernels (dh in {8, 16}, H * dh in {64, 128}), their
+ *   pairs run as dense 16 x 16 tiles on mma.sync and the rest of the pattern
+ *   on the sparse kernels; the two merge as online-softmax partials (forward)
+ *   and fixed-order partial sums (backward). Every sub-block must lie in the
+ *   plan's pattern and none may overlap (ConfigError otherwise). Sub-blocks
+ *   touching a row/column of degree > 1024 stay on the sparse path; other
+ *   d_b register nothing. n_used: sub-blocks executed as tiles.
+ * gte_plan_blocks: registered sub-blocks and the remainder's nnz. */
+int gte_plan_set_blocks(gte_plan* plan, int64_t n_blocks, const int64_t* origins, int64_t d_b, int64_t* n_used);
+int gte_plan_blocks(const gte_plan* plan, int64_t* n_blocks, int64_t* remainder_nnz);
+
 /* ---- sparse (topology-induced) attention over a plan, all heads at once ----
  * Replaces sparse_attention / sparse_attention_backward (reference
  * proj/src/attention.cpp:96-162, 241-320) called per head, and the per-head

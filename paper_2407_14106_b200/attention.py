@@ -192,6 +192,23 @@ class DevicePlan:
             raise ConfigError("plan: order length must equal the row count")
         check(_lib.lib().gte_plan_set_order(self.h, o.ctypes.data))
 
+    def set_blocks(self, origins, d_b: int = 16) -> int:
+        """Registers ECR sub-blocks (global (row0, col0) origins, side d_b;
+        ClusterSparseLayout.global_blocks()): with d_b == 16, bf16 calls run
+        their pairs as dense tiles on the tensor pipe (csrc/ecr_tile.cuh) and
+        the rest on the sparse kernels. Returns the number executed as tiles."""
+        o = np.ascontiguousarray(np.asarray(origins, dtype=np.int64).reshape(-1, 2))
+        used = C.c_int64()
+        check(_lib.lib().gte_plan_set_blocks(self.h, o.shape[0], o.ctypes.data if o.size else None, d_b,
+                                             C.byref(used)))
+        return used.value
+
+    def blocks(self):
+        """(registered sub-blocks, remainder nnz)."""
+        nb, rn = C.c_int64(), C.c_int64()
+        check(_lib.lib().gte_plan_blocks(self.h, C.byref(nb), C.byref(rn)))
+        return nb.value, rn.value
+
     def close(self):
         if self.h:
             _lib.lib().gte_plan_destroy(self.h)

@@ -72,6 +72,21 @@ struct SparseArgs {
   const int32_t* hubs_c = nullptr;
   int n_tiles = 0, n_hubs = 0, n_tiles_c = 0, n_hubs_c = 0;
   void* lsedelta = nullptr;
+  // ECR split (ecr_tile.cuh): the pattern here is the remainder of a layout
+  // whose dense sub-blocks ran on the tensor pipe. eid maps a CSR position to
+  // the original edge id (bias / weight_mult / dbias slots; the CSC view's
+  // csc_eid is already original). Per row (column) the tile partials to fold
+  // in are [inc_ptr[i], inc_ptr[i+1]) ([cinc_ptr[j], cinc_ptr[j+1])), rows of
+  // part_d floats: forward (m, l) in part_ml + unnormalised acc in part_acc;
+  // backward dQ in part_acc, dK / dV in part_dk / part_dv.
+  const int32_t* eid = nullptr;
+  const int32_t* inc_ptr = nullptr;
+  const int32_t* cinc_ptr = nullptr;
+  const float2* part_ml = nullptr;
+  const float* part_acc = nullptr;
+  const float* part_dk = nullptr;
+  const float* part_dv = nullptr;
+  int part_d = 0;
 };
 
 struct WarpRange {

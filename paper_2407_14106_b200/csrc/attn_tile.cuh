@@ -67,6 +67,8 @@ struct TileMeta {
   int pad[2];
 };
 
+// neighbour ids + biases (log2 units) of the staged edges; no more: the
+// shared-memory carve-out comes out of the L1 that serves the K/V gathers
 constexpr size_t tile_smem_bytes() { return sizeof(TileMeta) + (size_t)(kTileCap + kTilePad) * 8; }
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
   const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
@@ -88,8 +90,10 @@ __device__ __forceinline__ TileSmem tile_carve(unsigned char* raw) {
 }
 
 // Stage tile `blockIdx.x` of the pass. CSR pass: ptr = row_ptr, idx = cols,
-// eid = null, bias indexed by edge. CSC pass: ptr = col_ptr, idx = csc_row,
-// bias indexed by csc_eid. Returns the tile's row count; ends with a barrier.
+// eid = null (bias indexed by edge) or the ECR remainder's original edge ids.
+// CSC pass: ptr = col_ptr, idx = csc_row, eid = csc_eid. With eid the ids are
+// staged in the bias slots and replaced by the biases they point at. Returns
+// the tile's row count; ends with a barrier.
 __device__ __forceinline__ int tile_stage(TileMeta& mt, const TileSmem& s, const int32_t* __restrict__ order,
                                           const int32_t* __restrict__ tiles, const int32_t* __restrict__ ptr,
                                           const int32_t* __restrict__ idx, const int32_t* __restrict__ eid,
@@ -146,7 +150,7 @@ __device__ __forceinline__ int tile_stage(TileMeta& mt, const TileSmem& s, const
   __syncthreads();
   constexpr float kL2e = 1.4426950408889634f;
   if (bias) {
-    if (eid) {  // second hop: bias[csc_eid[e]], in log2 units
+    if (eid) {  // second hop: bias[eid[e]], in log2 units
       const int* ids = reinterpret_cast<const int*>(s.bias);
       for (int k = t; k < total; k += kTileThreads) s.bias[k] = __ldg(bias + ids[k]) * kL2e;
     } else {
@@ -245,7 +249,7 @@ __global__ void __launch_bounds__(kTileThreads, GTE_TILE_MINB) tile_fwd_kernel(S
   float* __restrict__ LSE = static_cast<float*>(p.lse);
   const uint32_t rq = (uint32_t)(p.ldq * sizeof(T)), rv = (uint32_t)(p.ldv * sizeof(T));
 
-  const int nrows = tile_stage(mt, sm, p.order, p.tiles, p.row_ptr, p.cols, nullptr,
+  const int nrows = tile_stage(mt, sm, p.order, p.tiles, p.row_ptr, p.cols, p.eid,
                                static_cast<const float*>(p.bias));
   float chk_q = 0.f, chk_k = 0.f, chk_v = 0.f;
   // own-row finiteness of K and V (attention.cpp:20-22): every non-hub row is
@@ -255,13 +259,14 @@ __global__ void __launch_bounds__(kTileThreads, GTE_TILE_MINB) tile_fwd_kernel(S
   __syncthreads();
 
   RowQueue<SLOTS, LPN> rq_{&mt.next, nrows};
-  int i = -1, k = 0, d = 0, ob = 0, gb = 0;
+  int i = -1, k = 0, d = 0, ob = 0, gb = 0, ninc = 0;
   uint4 q = make_uint4(0, 0, 0, 0);
   float m = M::neg_inf(), l = 0.f, acc[VW];
   auto start_row = [&](int r) {
     k = 0;
     m = M::neg_inf();
     l = 0.f;
+    ninc = 0;
 #pragma unroll
     for (int t = 0; t < VW; ++t) acc[t] = 0.f;
     if (r >= 0) {
@@ -270,6 +275,20 @@ __global__ void __launch_bounds__(kTileThreads, GTE_TILE_MINB) tile_fwd_kernel(S
       d = mt.off[r + 1] - ob;
       gb = mt.gbeg[r];
       q = ldg16(Q, (uint32_t)i * rq + g.bo);
+      if (p.inc_ptr) {  // ECR tile partials of this row: the running state starts from them
+        const int x0 = __ldg(p.inc_ptr + i), x1 = __ldg(p.inc_ptr + i + 1);
+        ninc = x1 - x0;
+        for (int x = x0; x < x1; ++x) {
+          const float2 ml = __ldg(p.part_ml + (int64_t)x * p.H + g.hcl);
+          const float mn = fmaxf(m, ml.x);
+          const float fa = M::ex(m - mn), fb = M::ex(ml.x - mn);
+          const float* pa = p.part_acc + (int64_t)x * p.part_d + g.hcl * p.dk + g.part * VW;
+          l = l * fa + ml.y * fb;
+#pragma unroll
+          for (int t = 0; t < VW; ++t) acc[t] = acc[t] * fa + __ldg(pa + t) * fb;
+          m = mn;
+        }
+      }
     } else {
       i = -1;
       ob = d = 0;
@@ -311,7 +330,7 @@ __global__ void __launch_bounds__(kTileThreads, GTE_TILE_MINB) tile_fwd_kernel(S
     for (int u = 0; u < EPL; ++u) {
       float pr = M::ex(s[u] - m_use);
       l += pr;
-      if (WM && u < rem) pr *= __ldg(wm + (int64_t)g.hcl * p.E + gb + k + u);
+      if (WM && u < rem) pr *= __ldg(wm + (int64_t)g.hcl * p.E + (p.eid ? __ldg(p.eid + gb + k + u) : gb + k + u));
       P::axpy_w(pr, vr[u], acc);
     }
     m = m_new;
@@ -320,7 +339,7 @@ __global__ void __launch_bounds__(kTileThreads, GTE_TILE_MINB) tile_fwd_kernel(S
     if (__any_sync(0xffffffffu, done)) {
       if (done) {
         if (g.head_ok) chk_q = P::finite_probe(q, chk_q);
-        if (d == 0) {  // empty row: zero output (attention.cpp:119-125)
+        if (d == 0 && ninc == 0) {  // empty row: zero output (attention.cpp:119-125)
           if (p.forbid_empty && (g.lane % LPN) == 0) atomicMin(p.err + 1, i);
           if (g.head_ok) {
             *reinterpret_cast<uint4*>(O + (uint32_t)i * rv + g.bo) = P::pack(acc);
@@ -369,7 +388,7 @@ __global__ void __launch_bounds__(kTileThreads, GTE_TILE_MINB) tile_bwd_rows_ker
   float* __restrict__ DB = static_cast<float*>(p.dbias);
   const uint32_t rq = (uint32_t)(p.ldq * sizeof(T)), rv = (uint32_t)(p.ldv * sizeof(T));
 
-  const int nrows = tile_stage(mt, sm, p.order, p.tiles, p.row_ptr, p.cols, nullptr,
+  const int nrows = tile_stage(mt, sm, p.order, p.tiles, p.row_ptr, p.cols, p.eid,
                                static_cast<const float*>(p.bias));
   float dummy_a = 0.f, dummy_b = 0.f;
   tile_own_rows<T, LPN, false>(mt, nrows, K, rq, Vp, rv, p.H * p.dk * (int)sizeof(T), dummy_a, dummy_b);
@@ -377,7 +396,7 @@ __global__ void __launch_bounds__(kTileThreads, GTE_TILE_MINB) tile_bwd_rows_ker
   __syncthreads();
 
   RowQueue<SLOTS, LPN> rq_{&mt.next, nrows};
-  int i = -1, k = 0, d = 0, ob = 0, gb = 0;
+  int i = -1, k = 0, d = 0, ob = 0, gb = 0, ninc = 0;
   uint4 q = make_uint4(0, 0, 0, 0), dd = q, oo = q;
   float lse = 0.f, delta = 0.f, dq[VW];
   auto start_row = [&](int r) {
@@ -389,6 +408,7 @@ __global__ void __launch_bounds__(kTileThreads, GTE_TILE_MINB) tile_bwd_rows_ker
       ob = mt.off[r];
       d = mt.off[r + 1] - ob;
       gb = mt.gbeg[r];
+      ninc = p.inc_ptr ? __ldg(p.inc_ptr + i + 1) - __ldg(p.inc_ptr + i) : 0;
       q = ldg16(Q, (uint32_t)i * rq + g.bo);
       dd = ldg16(DO, (uint32_t)i * rv + g.bo);
       oo = ldg16(O, (uint32_t)i * rv + g.bo);
@@ -421,7 +441,7 @@ __global__ void __launch_bounds__(kTileThreads, GTE_TILE_MINB) tile_bwd_rows_ker
       kr[u] = ldg16(K, j * rq + g.bo);
       vr[u] = ldg16(Vp, j * rv + g.bo);
     }
-    const bool single = d == 1;
+    const bool single = d == 1 && ninc == 0;
     // delta = dO_i . O_i is set at row start (row_delta); degree-1 rows take
     // the dw of their edge so ds == 0 exactly in both passes
     // (attention.cpp:265-272)
@@ -431,7 +451,7 @@ __global__ void __launch_bounds__(kTileThreads, GTE_TILE_MINB) tile_bwd_rows_ker
       const float sc = head_sum<LPH>(P::dot(q, kr[u]));
       float dw = head_sum<LPH>(P::dot(dd, vr[u]));
       const float pr = M::ex(__fmaf_rn(sc, scale_l, bl[u]) - lse);
-      if (WM && u < rem) dw = __fmul_rn(__ldg(wm + (int64_t)g.hcl * p.E + gb + k + u), dw);
+      if (WM && u < rem) dw = __fmul_rn(__ldg(wm + (int64_t)g.hcl * p.E + (p.eid ? __ldg(p.eid + gb + k + u) : gb + k + u)), dw);
       if (u == 0 && single && k == 0) delta = dw;
       const float ds = (u < rem && !single) ? pr * (dw - delta) : 0.f;
       P::axpy_w(ds, kr[u], dq);
@@ -442,14 +462,14 @@ __global__ void __launch_bounds__(kTileThreads, GTE_TILE_MINB) tile_bwd_rows_ker
         int which;
         bool owner;
         const float tot = EdgeReduce<EPL, LPN>::run(hs, g.lane % LPN, which, owner);
-        if (owner && i >= 0 && which < rem) DB[gb + k + which] = tot;
+        if (owner && i >= 0 && which < rem) DB[p.eid ? __ldg(p.eid + gb + k + which) : gb + k + which] = tot;
       } else {
 #pragma unroll
         for (int u = 0; u < EPL; ++u) {
           float hsum = hs[u];
 #pragma unroll
           for (int off = 1; off < LPN; off <<= 1) hsum += __shfl_xor_sync(0xffffffffu, hsum, off);
-          if (i >= 0 && u < rem && (g.lane % LPN) == 0) DB[gb + k + u] = hsum;
+          if (i >= 0 && u < rem && (g.lane % LPN) == 0) DB[p.eid ? __ldg(p.eid + gb + k + u) : gb + k + u] = hsum;
         }
       }
     }
@@ -457,6 +477,14 @@ __global__ void __launch_bounds__(kTileThreads, GTE_TILE_MINB) tile_bwd_rows_ker
     const bool done = i >= 0 && k >= d;
     if (__any_sync(0xffffffffu, done)) {
       if (done && g.head_ok) {
+        if (ninc) {  // ECR tile dQ partials, in incidence order
+          const int x0 = __ldg(p.inc_ptr + i);
+          for (int x = x0; x < x0 + ninc; ++x) {
+            const float* pa = p.part_acc + (int64_t)x * p.part_d + g.hcl * p.dk + g.part * VW;
+#pragma unroll
+            for (int t = 0; t < VW; ++t) dq[t] += __ldg(pa + t);
+          }
+        }
         const float sc = float(p.scale);
 #pragma unroll
         for (int t = 0; t < VW; ++t) dq[t] *= sc;
@@ -558,6 +586,17 @@ __global__ void __launch_bounds__(kTileThreads, GTE_TILE_MINB_COLS) tile_bwd_col
     const bool done = j >= 0 && k >= d;
     if (__any_sync(0xffffffffu, done)) {
       if (done && g.head_ok) {
+        if (p.cinc_ptr) {  // ECR tile dK / dV partials of this column, in incidence order
+          const int x1 = __ldg(p.cinc_ptr + j + 1);
+          for (int x = __ldg(p.cinc_ptr + j); x < x1; ++x) {
+            const int64_t o = (int64_t)x * p.part_d + g.hcl * p.dk + g.part * VW;
+#pragma unroll
+            for (int t = 0; t < VW; ++t) {
+              gk[t] += __ldg(p.part_dk + o + t);
+              gv[t] += __ldg(p.part_dv + o + t);
+            }
+          }
+        }
         const float sc = float(p.scale);
 #pragma unroll
         for (int t = 0; t < VW; ++t) gk[t] *= sc;
@@ -616,7 +655,8 @@ __global__ void __launch_bounds__(kTileThreads) hub_fwd_kernel(SparseArgs p) {
       const int e = e0 + u * NS;
       ok[u] = e < end;
       const uint32_t j = (uint32_t)__ldg(p.cols + (ok[u] ? e : beg));
-      bl[u] = (bias && ok[u]) ? __ldg(bias + e) * M::kLogScale : 0.f;
+      const int oe = (p.eid && ok[u]) ? __ldg(p.eid + e) : e;  // original edge id
+      bl[u] = (bias && ok[u]) ? __ldg(bias + oe) * M::kLogScale : 0.f;
       kr[u] = ldg16(K, j * rq + g.bo);
       vr[u] = ldg16(Vp, j * rv + g.bo);
     }
@@ -637,7 +677,7 @@ __global__ void __launch_bounds__(kTileThreads) hub_fwd_kernel(SparseArgs p) {
     for (int u = 0; u < EPL; ++u) {
       float pr = M::ex(s[u] - m_use);
       l += pr;
-      if (WM && ok[u]) pr *= __ldg(wm + (int64_t)g.hcl * p.E + e0 + u * NS);
+      if (WM && ok[u]) pr *= __ldg(wm + (int64_t)g.hcl * p.E + (p.eid ? __ldg(p.eid + e0 + u * NS) : e0 + u * NS));
       P::axpy_w(pr, vr[u], acc);
     }
     m = m_new;
@@ -714,12 +754,14 @@ __global__ void __launch_bounds__(kTileThreads) hub_bwd_rows_kernel(SparseArgs p
     uint4 kr[EPL], vr[EPL];
     float bl[EPL];
     bool ok[EPL];
+    int oe[EPL];
 #pragma unroll
     for (int u = 0; u < EPL; ++u) {
       const int e = e0 + u * NS;
       ok[u] = e < end;
       const uint32_t j = (uint32_t)__ldg(p.cols + (ok[u] ? e : beg));
-      bl[u] = (bias && ok[u]) ? __ldg(bias + e) * M::kLogScale : 0.f;
+      oe[u] = (p.eid && ok[u]) ? __ldg(p.eid + e) : e;  // original edge id
+      bl[u] = (bias && ok[u]) ? __ldg(bias + oe[u]) * M::kLogScale : 0.f;
       kr[u] = ldg16(K, j * rq + g.bo);
       vr[u] = ldg16(Vp, j * rv + g.bo);
     }
@@ -728,13 +770,13 @@ __global__ void __launch_bounds__(kTileThreads) hub_bwd_rows_kernel(SparseArgs p
       const float sc = head_sum<LPH>(P::dot(q, kr[u]));
       float dw = head_sum<LPH>(P::dot(dd, vr[u]));
       const float pr = M::ex(__fmaf_rn(sc, scale_l, bl[u]) - lse);
-      if (WM && ok[u]) dw = __fmul_rn(__ldg(wm + (int64_t)g.hcl * p.E + e0 + u * NS), dw);
+      if (WM && ok[u]) dw = __fmul_rn(__ldg(wm + (int64_t)g.hcl * p.E + oe[u]), dw);
       const float ds = ok[u] ? pr * (dw - delta) : 0.f;
       P::axpy_w(ds, kr[u], dq);
       float hsum = (g.part == 0 && g.head_ok) ? ds : 0.f;
 #pragma unroll
       for (int off = LPH; off < LPN; off <<= 1) hsum += __shfl_xor_sync(0xffffffffu, hsum, off);
-      if (DB && ok[u] && (g.lane % LPN) == 0) DB[e0 + u * NS] = hsum;
+      if (DB && ok[u] && (g.lane % LPN) == 0) DB[oe[u]] = hsum;
     }
   }
 #pragma unroll

@@ -13,6 +13,7 @@
 #include <cub/cub.cuh>
 
 #include "../../include/gte_b200.h"
+#include "ecr_tile.cuh"
 #include "tile_launch.cuh"
 
 using namespace gte_b200;
@@ -131,6 +132,22 @@ struct gte_ctx {
   DevBuf scratch;  // workspace of other translation units (ctx_scratch)
 };
 
+namespace gte_b200 {
+bool ecr_eligible(int H, int dk, int dv);
+cudaError_t launch_ecr_bf16(bool bwd, const EcrArgs& a, cudaStream_t st);
+}  // namespace gte_b200
+
+// ECR split of a plan (gte_plan_set_blocks): dense 16 x 16 sub-blocks on the
+// tensor pipe (ecr_tile.cuh) + the remainder pattern on the sparse kernels.
+struct EcrSplit {
+  int64_t n_blocks = 0, n_inc = 0, n_cinc = 0;
+  int32_t* dev = nullptr;  // one allocation: blk, ebase, inc, cinc, inc_ptr, cinc_ptr, eid
+  const int32_t *blk = nullptr, *ebase = nullptr, *inc = nullptr, *cinc = nullptr;
+  const int32_t *inc_ptr = nullptr, *cinc_ptr = nullptr, *eid = nullptr;
+  gte_plan* rem = nullptr;
+  DevBuf part;  // tile partials (forward: (m, l) + acc; backward: dQ, dK, dV)
+};
+
 struct gte_plan {
   gte_ctx* ctx = nullptr;
   int64_t rows = 0, nnz = 0, max_row_deg = 0, max_col_deg = 0, n_unref = 0;
@@ -148,6 +165,8 @@ struct gte_plan {
   int n_tiles = 0, n_hubs = 0, n_tiles_c = 0, n_hubs_c = 0;
   bool scheduled = false;
   int64_t communities = 0;
+  std::vector<int64_t> host_order;  // execution order given to gte_plan_set_order (empty: natural)
+  EcrSplit* ecr = nullptr;
 };
 
 namespace {
@@ -321,6 +340,13 @@ int build_exec(gte_plan* p, const int64_t* order) {
 
 void free_plan(gte_plan* p) {
   if (!p) return;
+  if (p->ecr) {
+    free_plan(p->ecr->rem);
+    cudaFree(p->ecr->dev);
+    p->ecr->part.release();
+    delete p->ecr;
+    p->ecr = nullptr;
+  }
   cudaFree(p->row_ptr);
   cudaFree(p->cols);
   cudaFree(p->col_ptr);
@@ -580,6 +606,152 @@ int gte_plan_set_order(gte_plan* p, const int64_t* order) {
   if (rc) return rc;
   p->scheduled = order != nullptr;
   if (!order) p->communities = 0;
+  if (order) p->host_order.assign(order, order + n);
+  else p->host_order.clear();
+  if (p->ecr && p->ecr->rem) return gte_plan_set_order(p->ecr->rem, order);
+  return GTE_OK;
+}
+
+// Registers the ECR sub-blocks of a cluster-sparse layout (global origins
+// (row0, col0), side d_b): their pairs run as dense tiles on the tensor pipe
+// (bf16, ecr_tile.cuh), the rest of the pattern on the sparse kernels. Every
+// sub-block must lie in the pattern as 16 contiguous column runs and no pair
+// may belong to two sub-blocks (the layout guarantees both:
+// reformation.cpp:82-99, 176-189). Sub-blocks touching a row or column of
+// degree > kHubDegree stay on the sparse path (hub kernels), and d_b != 16
+// registers nothing. Results do not depend on the split beyond rounding.
+int gte_plan_set_blocks(gte_plan* p, int64_t n_blocks, const int64_t* origins, int64_t d_b, int64_t* n_used) {
+  if (!p) return fail(GTE_CONFIG, "plan: null plan");
+  if (n_used) *n_used = 0;
+  if (p->ecr) {
+    free_plan(p->ecr->rem);
+    cudaFree(p->ecr->dev);
+    p->ecr->part.release();
+    delete p->ecr;
+    p->ecr = nullptr;
+  }
+  if (n_blocks < 0) return fail(GTE_CONFIG, "blocks: negative count");
+  if (n_blocks == 0 || d_b != kEcrDb) return GTE_OK;
+  const int64_t n = p->rows, m = p->nnz;
+  cudaStream_t st = p->ctx->stream;
+  std::vector<int32_t> rp(n + 1), cl(m > 0 ? m : 1), cp(n + 1);
+  CUDA_TRY(cudaMemcpyAsync(rp.data(), p->row_ptr, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(cp.data(), p->col_ptr, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost, st));
+  if (m) CUDA_TRY(cudaMemcpyAsync(cl.data(), p->cols, sizeof(int32_t) * m, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  std::vector<char> taken(m > 0 ? m : 1, 0);
+  std::vector<int32_t> blk, ebase;
+  for (int64_t b = 0; b < n_blocks; ++b) {
+    const int64_t r0 = origins[2 * b], c0 = origins[2 * b + 1];
+    if (r0 < 0 || c0 < 0 || r0 + d_b > n || c0 + d_b > n)
+      return fail(GTE_CONFIG, "blocks: sub-block outside the sequence");
+    bool hub = false;
+    for (int64_t t = 0; t < d_b; ++t)
+      hub |= rp[r0 + t + 1] - rp[r0 + t] > kHubDegree || cp[c0 + t + 1] - cp[c0 + t] > kHubDegree;
+    int32_t eb[kEcrDb];
+    for (int64_t t = 0; t < d_b; ++t) {
+      const int32_t* b0 = cl.data() + rp[r0 + t];
+      const int32_t* b1 = cl.data() + rp[r0 + t + 1];
+      const int32_t* at = std::lower_bound(b0, b1, (int32_t)c0);
+      if (b1 - at < d_b || at[d_b - 1] != (int32_t)(c0 + d_b - 1))
+        return fail(GTE_CONFIG, "blocks: sub-block (" + std::to_string(r0) + ", " + std::to_string(c0) +
+                                    ") is not inside the pattern");
+      eb[t] = (int32_t)(at - cl.data());
+    }
+    if (hub) continue;
+    for (int64_t t = 0; t < d_b; ++t)
+      for (int64_t u = 0; u < d_b; ++u) {
+        if (taken[eb[t] + u]) return fail(GTE_CONFIG, "blocks: sub-blocks overlap");
+        taken[eb[t] + u] = 1;
+      }
+    blk.push_back((int32_t)r0);
+    blk.push_back((int32_t)c0);
+    ebase.insert(ebase.end(), eb, eb + d_b);
+  }
+  const int64_t nb = (int64_t)blk.size() / 2;
+  if (nb == 0) return GTE_OK;
+  // incidences: per row (column) the sub-blocks covering it, in block order
+  std::vector<int32_t> inc_ptr(n + 1, 0), cinc_ptr(n + 1, 0), inc(nb * d_b), cinc(nb * d_b);
+  for (int64_t b = 0; b < nb; ++b)
+    for (int64_t t = 0; t < d_b; ++t) {
+      inc_ptr[blk[2 * b] + t + 1]++;
+      cinc_ptr[blk[2 * b + 1] + t + 1]++;
+    }
+  for (int64_t i = 0; i < n; ++i) {
+    inc_ptr[i + 1] += inc_ptr[i];
+    cinc_ptr[i + 1] += cinc_ptr[i];
+  }
+  {
+    std::vector<int32_t> fr(inc_ptr.begin(), inc_ptr.end() - 1), fc(cinc_ptr.begin(), cinc_ptr.end() - 1);
+    for (int64_t b = 0; b < nb; ++b)
+      for (int64_t t = 0; t < d_b; ++t) {
+        inc[b * d_b + t] = fr[blk[2 * b] + t]++;
+        cinc[b * d_b + t] = fc[blk[2 * b + 1] + t]++;
+      }
+  }
+  // remainder pattern (CSR positions -> original edge ids)
+  std::vector<int64_t> rro(n + 1, 0), rco;
+  std::vector<int32_t> eid;
+  rco.reserve(m);
+  eid.reserve(m);
+  for (int64_t i = 0; i < n; ++i) {
+    for (int64_t e = rp[i]; e < rp[i + 1]; ++e)
+      if (!taken[e]) {
+        rco.push_back(cl[e]);
+        eid.push_back((int32_t)e);
+      }
+    rro[i + 1] = (int64_t)rco.size();
+  }
+  auto* x = new EcrSplit();
+  x->n_blocks = nb;
+  x->n_inc = inc_ptr[n];
+  x->n_cinc = cinc_ptr[n];
+  const int64_t mr = (int64_t)rco.size();
+  int rc = gte_plan_create_host(p->ctx, n, mr, rro.data(), mr ? rco.data() : rro.data(), &x->rem);
+  if (rc) {
+    delete x;
+    return rc;
+  }
+  p->ecr = x;
+  if (!p->host_order.empty()) {
+    rc = gte_plan_set_order(x->rem, p->host_order.data());
+    if (rc) return rc;
+  }
+  // the remainder's CSC edge ids -> original edge ids
+  if (mr) {
+    std::vector<int32_t> ce(mr);
+    CUDA_TRY(cudaMemcpyAsync(ce.data(), x->rem->csc_eid, sizeof(int32_t) * mr, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    for (auto& v : ce) v = eid[v];
+    CUDA_TRY(cudaMemcpyAsync(x->rem->csc_eid, ce.data(), sizeof(int32_t) * mr, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+  }
+  const size_t total = blk.size() + ebase.size() + inc.size() + cinc.size() + 2 * (n + 1) + eid.size() + 1;
+  CUDA_TRY(cudaMalloc(&x->dev, sizeof(int32_t) * total));
+  int32_t* cur = x->dev;
+  auto put = [&](const std::vector<int32_t>& v, const int32_t** where) -> cudaError_t {
+    *where = cur;
+    cudaError_t e = v.empty() ? cudaSuccess
+                              : cudaMemcpyAsync(cur, v.data(), sizeof(int32_t) * v.size(), cudaMemcpyHostToDevice, st);
+    cur += v.size();
+    return e;
+  };
+  CUDA_TRY(put(blk, &x->blk));
+  CUDA_TRY(put(ebase, &x->ebase));
+  CUDA_TRY(put(inc, &x->inc));
+  CUDA_TRY(put(cinc, &x->cinc));
+  CUDA_TRY(put(inc_ptr, &x->inc_ptr));
+  CUDA_TRY(put(cinc_ptr, &x->cinc_ptr));
+  CUDA_TRY(put(eid, &x->eid));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (n_used) *n_used = nb;
+  return GTE_OK;
+}
+
+int gte_plan_blocks(const gte_plan* p, int64_t* n_blocks, int64_t* remainder_nnz) {
+  if (!p) return fail(GTE_CONFIG, "plan: null plan");
+  if (n_blocks) *n_blocks = p->ecr ? p->ecr->n_blocks : 0;
+  if (remainder_nnz) *remainder_nnz = p->ecr ? p->ecr->rem->nnz : p->nnz;
   return GTE_OK;
 }
 
@@ -602,6 +774,43 @@ int gte_plan_schedule(gte_plan* p, int64_t iters, int64_t* communities) {
   return GTE_OK;
 }
 
+namespace {
+
+// The ECR split runs when sub-blocks are registered, the tile path is taken,
+// the dtype is bf16 (tensor-core tiles) and the head geometry has kernels.
+EcrSplit* ecr_split_for(const gte_plan* plan, int dtype, int lph, int H, int dk, int dv) {
+  EcrSplit* x = plan->ecr;
+  if (!x || x->n_blocks == 0 || !lph || dtype != GTE_BF16 || !ecr_eligible(H, dk, dv)) return nullptr;
+  return x;
+}
+
+cudaError_t ecr_prepare(EcrSplit* x, const gte_plan* plan, int H, int dk, int64_t ldq, int64_t ldv, EcrArgs& e,
+                        SparseArgs& a2, float** part) {
+  const size_t D = (size_t)H * dk;
+  const size_t fwd = (size_t)x->n_inc * (2 * H + D), bwd = (size_t)x->n_inc * D + 2 * (size_t)x->n_cinc * D;
+  cudaError_t err = x->part.ensure(sizeof(float) * (fwd > bwd ? fwd : bwd));
+  if (err != cudaSuccess) return err;
+  *part = static_cast<float*>(x->part.p);
+  e.n_blocks = (int)x->n_blocks;
+  e.H = H;
+  e.dh = dk;
+  e.E = plan->nnz;
+  e.ldq = ldq;
+  e.ldv = ldv;
+  e.scale = (float)(1.0 / std::sqrt((double)dk));
+  e.blk = x->blk;
+  e.ebase = x->ebase;
+  e.inc = x->inc;
+  e.cinc = x->cinc;
+  a2.E = plan->nnz;  // weight_mult rows stay [H][E] of the full pattern
+  a2.eid = x->eid;
+  a2.inc_ptr = x->inc_ptr;
+  a2.part_d = (int)D;
+  return cudaSuccess;
+}
+
+}  // namespace
+
 int gte_sparse_attn_fwd(gte_ctx* c, const gte_plan* plan, int dtype, int H, int dk, int dv,
                         const void* q, const void* k, int64_t ldq, const void* v, int64_t ldv,
                         const void* bias, const void* wmult, void* out, void* lse, int flags) {
@@ -623,7 +832,26 @@ int gte_sparse_attn_fwd(gte_ctx* c, const gte_plan* plan, int dtype, int H, int 
   a.vec_v = dv == dht && (ldv * es) % 16 == 0 && aligned16(v) && aligned16(out);
   if (plan->rows == 0) return GTE_OK;
   const int lph = fast_lph(dtype, plan->rows, H, dk, dv, ldq, ldv, {q, k, v, out});
-  if (lph) {
+  if (EcrSplit* x = ecr_split_for(plan, dtype, lph, H, dk, dv)) {
+    // ECR: dense sub-blocks on the tensor pipe, then the remainder folds their partials in
+    EcrArgs e;
+    SparseArgs a2 = a;
+    fill_common(a2, x->rem, dtype, H, dk, dv, ldq, ldv);
+    float* part = nullptr;
+    CUDA_TRY(ecr_prepare(x, plan, H, dk, ldq, ldv, e, a2, &part));
+    e.q = q;
+    e.k = k;
+    e.v = v;
+    e.bias = static_cast<const float*>(bias);
+    e.wmult = static_cast<const float*>(wmult);
+    e.part_ml = reinterpret_cast<float2*>(part);
+    e.part_acc = part + 2 * (size_t)H * x->n_inc;
+    CUDA_TRY(launch_ecr_bf16(false, e, c->stream));
+    c->launches += 1;
+    a2.part_ml = e.part_ml;
+    a2.part_acc = e.part_acc;
+    CUDA_TRY(dispatch_tile(dtype, kFwd, a2, lph, c->stream, &c->launches));
+  } else if (lph) {
     CUDA_TRY(dispatch_tile(dtype, kFwd, a, lph, c->stream, &c->launches));
   } else {
     CUDA_TRY(dispatch(dtype, kFwd, a, dht, lpn, c->stream));
@@ -669,7 +897,36 @@ int gte_sparse_attn_bwd(gte_ctx* c, const gte_plan* plan, int dtype, int H, int 
   a.vec_qk = dk == dht && (ldq * es) % 16 == 0 && aligned16(q) && aligned16(k) && aligned16(dq) && aligned16(dk_out);
   a.vec_v = dv == dht && (ldv * es) % 16 == 0 && aligned16(v) && aligned16(out) && aligned16(dout) && aligned16(dv_out);
   const int lph = fast_lph(dtype, plan->rows, H, dk, dv, ldq, ldv, {q, k, v, out, dout, dq, dk_out, dv_out});
-  if (lph) {
+  if (EcrSplit* x = ecr_split_for(plan, dtype, lph, H, dk, dv)) {
+    // ECR: sub-block partials (dQ rows, dK/dV columns, final dbias of their
+    // pairs) first, then the remainder's two passes add them in
+    EcrArgs e;
+    SparseArgs a2 = a;
+    fill_common(a2, x->rem, dtype, H, dk, dv, ldq, ldv);
+    float* part = nullptr;
+    CUDA_TRY(ecr_prepare(x, plan, H, dk, ldq, ldv, e, a2, &part));
+    const size_t D = (size_t)H * dk;
+    e.q = q;
+    e.k = k;
+    e.v = v;
+    e.o = out;
+    e.dout = dout;
+    e.bias = static_cast<const float*>(bias);
+    e.wmult = static_cast<const float*>(wmult);
+    e.lse = static_cast<const float*>(lse);
+    e.part_acc = part;
+    e.part_dk = part + D * x->n_inc;
+    e.part_dv = e.part_dk + D * x->n_cinc;
+    e.dbias = static_cast<float*>(dbias);
+    CUDA_TRY(launch_ecr_bf16(true, e, c->stream));
+    c->launches += 1;
+    a2.cinc_ptr = x->cinc_ptr;
+    a2.part_acc = e.part_acc;
+    a2.part_dk = e.part_dk;
+    a2.part_dv = e.part_dv;
+    CUDA_TRY(dispatch_tile(dtype, kBwdRows, a2, lph, c->stream, &c->launches));
+    CUDA_TRY(dispatch_tile(dtype, kBwdCols, a2, lph, c->stream, &c->launches));
+  } else if (lph) {
     CUDA_TRY(dispatch_tile(dtype, kBwdRows, a, lph, c->stream, &c->launches));
     CUDA_TRY(dispatch_tile(dtype, kBwdCols, a, lph, c->stream, &c->launches));
   } else {

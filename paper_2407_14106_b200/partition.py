@@ -86,6 +86,19 @@ class ClusterSparseLayout:
     def subblock_count(self) -> int:
         return int(self.blocks.shape[0])
 
+    def global_blocks(self) -> np.ndarray:
+        """Sub-block origins in sequence coordinates, [n_blocks, 2] (row0, col0),
+        cell by cell (reformation.cpp:176-189 places tile (r, c) of cell (a, b)
+        at (boundaries[a] + r, boundaries[b] + c))."""
+        out = np.zeros((int(self.block_off[-1]), 2), dtype=np.int64)
+        for cell in range(self.k * self.k):
+            b0, b1 = int(self.block_off[cell]), int(self.block_off[cell + 1])
+            if b1 > b0:
+                a, b = divmod(cell, self.k)
+                out[b0:b1, 0] = self.blocks[b0:b1, 0] + self.boundaries[a]
+                out[b0:b1, 1] = self.blocks[b0:b1, 1] + self.boundaries[b]
+        return out
+
     def cell_blocks(self, cell: int) -> np.ndarray:
         return self.blocks[self.block_off[cell]:self.block_off[cell + 1]]
 

@@ -69,7 +69,7 @@ def _torch_dtype(dtype):
     return {"f64": torch.float64, "f32": torch.float32, "bf16": torch.bfloat16}[dtype]
 
 
-def run_device(row_off, cols, H, dh, dtype, seed=0, with_bias=True, with_wm=False, S=None, order=None):
+def run_device(row_off, cols, H, dh, dtype, seed=0, with_bias=True, with_wm=False, S=None, order=None, blocks=None):
     """Runs fwd+bwd through DeviceSparseAttention; returns the dtype-rounded fp64
     inputs and the outputs, as numpy fp64."""
     import torch
@@ -88,13 +88,14 @@ def run_device(row_off, cols, H, dh, dtype, seed=0, with_bias=True, with_wm=Fals
         plan.schedule()
     elif order is not None:
         plan.set_order(order)
+    tiles = plan.set_blocks(blocks, 16) if blocks is not None else 0
     att = A.DeviceSparseAttention(plan, H, dh, dh, dtype)
     out, lse = att.forward(q, k, v, bias, wm)
     dq, dk, dv, db = att.backward(q, k, v, out, lse, do, bias, wm)
     plan.ctx.sync()
     f = lambda t: None if t is None else t.double().cpu().numpy()  # noqa: E731
     return dict(q=f(q), k=f(k), v=f(v), do=f(do), bias=f(bias), wm=f(wm), out=f(out), dq=f(dq), dk=f(dk), dv=f(dv),
-                db=f(db)[:E], lse=f(lse))
+                db=f(db)[:E], lse=f(lse), tiles=tiles)
 
 
 def oracle_multihead(orc, g: CSR, r, H, dh):
