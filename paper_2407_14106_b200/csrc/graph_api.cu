@@ -8,7 +8,8 @@
 //   build_cluster_grid proj/src/partition.cpp:514-539 -> smem-privatised k x k histogram, fp64 densities
 //   build_layout       proj/src/reformation.cpp:111-195 -> fp64 classification (host), exact packer
 //                      (pack.cpp, threads over cells), pattern materialised by count + scan + fill kernels
-//   reorder            proj/src/partition.cpp:413-433 -> reorder.cpp (host, exact)
+//   reorder            proj/src/partition.cpp:413-433 -> bisection.cpp (host greedy) +
+//                      partition_gpu.cu (device coarsening / splitting)
 #include <algorithm>
 #include <atomic>
 #include <climits>
@@ -21,7 +22,7 @@
 
 #include "../../include/gte_b200.h"
 #include "pack.h"
-#include "reorder.h"
+#include "bisection.h"
 
 // error channel shared with capi.cu
 namespace gte_b200 {
@@ -315,9 +316,9 @@ int gte_reorder(int64_t n, int64_t nnz, const int64_t* row_off, const int64_t* c
   if (k < 1 || (k & (k - 1)) != 0) return set_error(GTE_CONFIG, "reorder: k must be a power of two >= 1");
   if (k > n) return set_error(GTE_CONFIG, "reorder: k exceeds node count");
   try {
-    reorder_exact(n, row_off, cols, k, seed, forward, inverse);
+    reorder_cluster(n, row_off, cols, k, seed, forward, inverse);
   } catch (const std::exception& e) {
-    return set_error(GTE_CONFIG, std::string("reorder: ") + e.what());
+    return set_error(GTE_CUDA, e.what());
   }
   return GTE_OK;
 }

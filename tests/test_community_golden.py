@@ -9,7 +9,7 @@ and the layout built from it by the oracle's candidate-origin packer (the
 reference packer cannot run at C3; the candidate packer is itself pinned to
 the reference below and at 16K/32K/64K).
 
-reorder (host C++) and the oracle run without a GPU; the product's grid,
+the oracle runs without a GPU; the product's reorder (device coarsening), grid,
 permutation and layout builders run on the GPU (marked gpu).
 """
 import hashlib
@@ -51,6 +51,7 @@ def _G(n, ro, co):
     return Graph(n, np.asarray(ro, np.int64), np.asarray(co, np.int64))
 
 
+@pytest.mark.gpu
 @pytest.mark.parametrize("name", SIZES + ["c3"])
 def test_reorder_matches_reference(name):
     """Product reorder (csrc/reorder.cpp) == reference reorder, bit for bit."""
@@ -120,6 +121,8 @@ def test_layout_matches_reference(cuda, name):
     assert np.array_equal(perm.forward, d["reorder_fwd"].astype(np.int64))
     assert np.array_equal(grid.cell_nnz, d["grid_nnz"]) and np.array_equal(grid.cell_density, d["grid_den"])
     assert fnv1a64_fast(gp.col_indices) == str(d["gperm_cols_fnv"])
+    if "L5bg_state" not in d:  # the reference layout did not finish at this size (comm64k)
+        return
     assert np.array_equal(L.cell_state, d["L5bg_state"])
     assert np.array_equal(L.block_off, d["L5bg_boff"]) and np.array_equal(L.blocks, d["L5bg_blocks"])
     assert L.dropped_edges == int(d["L5bg_dropped"]) and L.pattern.nnz() == int(d["L5bg_pnnz"])
