@@ -267,6 +267,34 @@ int gte_pattern_buckets(gte_ctx* ctx, int64_t rows, int64_t nnz, const int32_t* 
                         int64_t max_dist, int32_t* d_buckets);
 int gte_bias_from_table(gte_ctx* ctx, int64_t nnz, const int32_t* d_buckets, const float* d_table, int64_t n_buckets,
                         float* d_bias);
+
+/* ---- SPD buckets on the GPU (reference spd_table,
+ * graph.cpp:208-261, without its N <= 20000 guard) ----
+ * Graph: device int32 CSR of the reference Graph (arcs traversed both ways,
+ * self loops ignored). Distances beyond max_dist (or unreachable) are
+ * max_dist + 1 (SpdTable::unreachable_bucket).
+ * gte_spd_table: the reference's table (rows = sources, columns ascending,
+ *   uint16 distances <= max_dist), one capped BFS per source on the device;
+ *   gte_spd_info / gte_spd_copy_host read it back (int64 row_off [n + 1],
+ *   int64 cols, uint16 dist [total]).
+ * gte_spd_pairs: distances of n_pairs (src, dst) pairs without the table
+ *   (radius-2 balls + min-plus meet in the middle, early-exit BFS for the
+ *   pairs beyond 4 hops); d_dist int32.
+ * gte_pattern_buckets_graph: the Trainer's bucket per attended pair
+ *   (model.cpp:447-463) with SPD from the graph itself: same rules as
+ *   gte_pattern_buckets, lookup replaced by gte_spd_pairs. */
+typedef struct gte_spd gte_spd;
+int gte_spd_table(gte_ctx* ctx, int64_t n, int64_t nnz, const int32_t* d_row_ptr, const int32_t* d_cols,
+                  int64_t max_dist, gte_spd** out);
+int gte_spd_info(const gte_spd* t, int64_t* n, int64_t* max_dist, int64_t* total);
+int gte_spd_copy_host(const gte_spd* t, int64_t* row_off, int64_t* cols, uint16_t* dist);
+int gte_spd_destroy(gte_spd* t);
+int gte_spd_pairs(gte_ctx* ctx, int64_t n, int64_t nnz, const int32_t* d_row_ptr, const int32_t* d_cols,
+                  int64_t max_dist, int64_t n_pairs, const int32_t* d_src, const int32_t* d_dst, int32_t* d_dist);
+int gte_pattern_buckets_graph(gte_ctx* ctx, int64_t rows, int64_t nnz, const int32_t* d_row_ptr,
+                              const int32_t* d_cols, const int64_t* d_perm_inverse, int64_t global_index,
+                              int64_t graph_n, int64_t graph_nnz, const int32_t* d_graph_row_ptr,
+                              const int32_t* d_graph_cols, int64_t max_dist, int32_t* d_buckets);
 int gte_dbias_to_table(gte_ctx* ctx, int64_t nnz, const int32_t* d_buckets, const float* d_dbias, int64_t n_buckets,
                        float* d_table_grad, float* d_workspace);
 

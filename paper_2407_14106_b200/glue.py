@@ -23,6 +23,12 @@ def _bind():
         L.gte_pattern_buckets.argtypes = [VP, I64, I64, VP, VP, VP, I64, I64, VP, VP, VP, I64, VP]
         L.gte_bias_from_table.argtypes = [VP, I64, VP, VP, I64, VP]
         L.gte_dbias_to_table.argtypes = [VP, I64, VP, VP, I64, VP, VP]
+        L.gte_spd_table.argtypes = [VP, I64, I64, VP, VP, I64, C.POINTER(VP)]
+        L.gte_spd_info.argtypes = [VP, C.POINTER(I64), C.POINTER(I64), C.POINTER(I64)]
+        L.gte_spd_copy_host.argtypes = [VP, VP, VP, VP]
+        L.gte_spd_destroy.argtypes = [VP]
+        L.gte_spd_pairs.argtypes = [VP, I64, I64, VP, VP, I64, I64, VP, VP, VP]
+        L.gte_pattern_buckets_graph.argtypes = [VP, I64, I64, VP, VP, VP, I64, I64, I64, VP, VP, I64, VP]
         L._glue_bound = True
     return L
 
@@ -84,3 +90,70 @@ def dbias_to_table(buckets, dbias, n_buckets: int, ctx: Context | None = None):
     check(_bind().gte_dbias_to_table(ctx.h, buckets.numel(), buckets.data_ptr(), dbias.data_ptr(), n_buckets,
                                      out.data_ptr(), ws.data_ptr()))
     return out
+
+
+def _dev_csr(row_offsets, cols, dev):
+    import torch
+
+    ro = torch.tensor(np.asarray(row_offsets, dtype=np.int32), device=dev)
+    co = np.asarray(cols, dtype=np.int32)
+    co = torch.tensor(co if co.shape[0] else np.zeros(1, np.int32), device=dev)
+    return ro, co, int(np.asarray(cols).shape[0])
+
+
+def spd_table(row_offsets, cols, max_dist: int, ctx: Context | None = None):
+    """The reference SpdTable (graph.cpp:216-262) built on the GPU, any size
+    whose table fits: (row_off int64, cols int64, dist uint16, num_nodes)."""
+    ctx = ctx or Context.get(0)
+    import torch
+
+    dev = torch.device("cuda", ctx.device)
+    ro, co, m = _dev_csr(row_offsets, cols, dev)
+    n = ro.numel() - 1
+    h = VP()
+    L = _bind()
+    check(L.gte_spd_table(ctx.h, n, m, ro.data_ptr(), co.data_ptr(), max_dist, C.byref(h)))
+    try:
+        nn, md, tot = I64(), I64(), I64()
+        L.gte_spd_info(h, C.byref(nn), C.byref(md), C.byref(tot))
+        sro = np.zeros(n + 1, np.int64)
+        sco = np.zeros(max(tot.value, 1), np.int64)
+        sdi = np.zeros(max(tot.value, 1), np.uint16)
+        check(L.gte_spd_copy_host(h, sro.ctypes.data, sco.ctypes.data, sdi.ctypes.data))
+        return sro, sco[: tot.value], sdi[: tot.value], n
+    finally:
+        L.gte_spd_destroy(h)
+
+
+def spd_pairs(row_offsets, cols, max_dist: int, src, dst, ctx: Context | None = None):
+    """Capped shortest-path distance of each (src, dst) pair on the GPU,
+    without the table (max_dist + 1 beyond the cap); int32 numpy."""
+    ctx = ctx or Context.get(0)
+    import torch
+
+    dev = torch.device("cuda", ctx.device)
+    ro, co, m = _dev_csr(row_offsets, cols, dev)
+    s = torch.tensor(np.asarray(src, np.int32), device=dev)
+    d = torch.tensor(np.asarray(dst, np.int32), device=dev)
+    out = torch.empty(max(s.numel(), 1), dtype=torch.int32, device=dev)
+    check(_bind().gte_spd_pairs(ctx.h, ro.numel() - 1, m, ro.data_ptr(), co.data_ptr(), max_dist, s.numel(),
+                                s.data_ptr(), d.data_ptr(), out.data_ptr()))
+    return out[: s.numel()].cpu().numpy()
+
+
+def pattern_buckets_graph(row_offsets, cols, perm_inverse, global_index: int, graph_row_offsets, graph_cols,
+                          max_dist: int, ctx: Context | None = None):
+    """Bucket per attended pair (model.cpp:447-463) with the SPD computed from
+    the graph on the GPU (no N <= 20000 table guard). int32 CUDA tensor."""
+    ctx = ctx or Context.get(0)
+    import torch
+
+    dev = torch.device("cuda", ctx.device)
+    ro, co, m = _dev_csr(row_offsets, cols, dev)
+    gro, gco, gm = _dev_csr(graph_row_offsets, graph_cols, dev)
+    inv = torch.tensor(np.asarray(perm_inverse, dtype=np.int64), device=dev)
+    out = torch.empty(max(m, 1), dtype=torch.int32, device=dev)
+    check(_bind().gte_pattern_buckets_graph(ctx.h, ro.numel() - 1, m, ro.data_ptr(), co.data_ptr(), inv.data_ptr(),
+                                            global_index, gro.numel() - 1, gm, gro.data_ptr(), gco.data_ptr(),
+                                            max_dist, out.data_ptr()))
+    return out[:m]
