@@ -243,6 +243,29 @@ int gte_dense_attn_bwd(gte_ctx* ctx, int dtype, int64_t S, int64_t s_real, int H
                        const void* k, int64_t ldq, const void* v, int64_t ldv, const void* out, const void* lse,
                        const void* dout, const void* bias, const void* wmult, void* dq, void* dk_out, void* dv_out,
                        void* dbias);
+/* Bucket-bias form of the Trainer's dense epoch (model.cpp:395-423, 520-523):
+ * bias[r][c] = table[buckets[r][c]] with uint8 buckets [S x S] (execution
+ * coordinates, gte_dense_buckets) and a table of n_buckets (<= 12) values of
+ * the accumulate type; the backward returns the table's gradient dtable
+ * [n_buckets] (dbias summed per bucket and over heads, fixed order) instead of
+ * an S x S dbias. */
+int gte_dense_attn_fwd_buckets(gte_ctx* ctx, int dtype, int64_t S, int64_t s_real, int H, int dk, int dv,
+                               const void* q, const void* k, int64_t ldq, const void* v, int64_t ldv,
+                               const uint8_t* buckets, const void* table, int64_t n_buckets, const void* wmult,
+                               void* out, void* lse);
+int gte_dense_attn_bwd_buckets(gte_ctx* ctx, int dtype, int64_t S, int64_t s_real, int H, int dk, int dv,
+                               const void* q, const void* k, int64_t ldq, const void* v, int64_t ldv, const void* out,
+                               const void* lse, const void* dout, const uint8_t* buckets, const void* table,
+                               int64_t n_buckets, const void* wmult, void* dq, void* dk_out, void* dv_out,
+                               void* dtable);
+/* gte_dense_buckets: the bucket matrix of a dense epoch (model.cpp:407-423):
+ * rows r < s_real (execution coordinates) of d_out [S x S]: 0 self, 1 to/from
+ * the global token (global_index, or -1), else the capped SPD of the original
+ * nodes over the graph (max_dist + 1 beyond the cap), one BFS per row on the
+ * device. perm forward [s_real], inverse [S] (int64, device). */
+int gte_dense_buckets(gte_ctx* ctx, int64_t S, int64_t s_real, const int64_t* d_perm_forward,
+                      const int64_t* d_perm_inverse, int64_t global_index, int64_t graph_n, int64_t graph_nnz,
+                      const int32_t* d_graph_row_ptr, const int32_t* d_graph_cols, int64_t max_dist, uint8_t* d_out);
 int gte_dense_attn_fwd_host(gte_ctx* ctx, int dtype, int64_t S, int64_t s_real, int H, int dk, int dv, const void* q,
                             const void* k, const void* v, const void* bias, const void* wmult, void* out, void* lse);
 int gte_dense_attn_bwd_host(gte_ctx* ctx, int dtype, int64_t S, int64_t s_real, int H, int dk, int dv, const void* q,

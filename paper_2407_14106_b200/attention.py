@@ -467,6 +467,10 @@ def _bind_dense():
                                               VPt]
         L.gte_dense_attn_bwd_host.argtypes = [VPt, I32t, I64t, I64t, I32t, I32t, I32t, VPt, VPt, VPt, VPt, VPt, VPt,
                                               VPt, VPt, VPt, VPt]
+        L.gte_dense_attn_fwd_buckets.argtypes = [VPt, I32t, I64t, I64t, I32t, I32t, I32t, VPt, VPt, I64t, VPt, I64t,
+                                                 VPt, VPt, I64t, VPt, VPt, VPt]
+        L.gte_dense_attn_bwd_buckets.argtypes = [VPt, I32t, I64t, I64t, I32t, I32t, I32t, VPt, VPt, I64t, VPt, I64t,
+                                                 VPt, VPt, VPt, VPt, VPt, I64t, VPt, VPt, VPt, VPt, VPt]
         L._dense_bound = True
     return L
 
@@ -563,3 +567,36 @@ class DeviceDenseAttention:
                                    None if weight_mult is None else weight_mult.data_ptr(), dq.data_ptr(),
                                    dk.data_ptr(), dv.data_ptr(), None if db is None else db.data_ptr()))
         return dq, dk, dv, db
+
+    # bucket-bias form of the Trainer's dense epoch (model.cpp:395-423, 520-523):
+    # bias[r][c] = table[buckets[r][c]] (uint8 [S, S], glue.dense_buckets); the
+    # backward returns the table's gradient instead of an S x S dbias
+    def forward_buckets(self, q, k, v, buckets, table, weight_mult=None):
+        import torch
+
+        L = _bind_dense()
+        acc = torch.float64 if self.dtype == "f64" else torch.float32
+        out = torch.empty((self.S, self.H * self.dv), dtype=v.dtype, device=v.device)
+        lse = torch.empty((self.S, self.H), dtype=acc, device=v.device)
+        self.ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+        check(L.gte_dense_attn_fwd_buckets(self.ctx.h, self.code, self.S, self.s_real, self.H, self.dk, self.dv,
+                                           q.data_ptr(), k.data_ptr(), q.stride(0), v.data_ptr(), v.stride(0),
+                                           buckets.data_ptr(), table.data_ptr(), table.numel(),
+                                           None if weight_mult is None else weight_mult.data_ptr(), out.data_ptr(),
+                                           lse.data_ptr()))
+        return out, lse
+
+    def backward_buckets(self, q, k, v, out, lse, dout, buckets, table, weight_mult=None):
+        import torch
+
+        L = _bind_dense()
+        dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+        dtable = torch.empty_like(table)
+        self.ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+        check(L.gte_dense_attn_bwd_buckets(self.ctx.h, self.code, self.S, self.s_real, self.H, self.dk, self.dv,
+                                           q.data_ptr(), k.data_ptr(), q.stride(0), v.data_ptr(), v.stride(0),
+                                           out.data_ptr(), lse.data_ptr(), dout.data_ptr(), buckets.data_ptr(),
+                                           table.data_ptr(), table.numel(),
+                                           None if weight_mult is None else weight_mult.data_ptr(), dq.data_ptr(),
+                                           dk.data_ptr(), dv.data_ptr(), dtable.data_ptr()))
+        return dq, dk, dv, dtable

@@ -85,12 +85,20 @@ template <> struct DMath<double> {
   __device__ static double ninf() { return -INFINITY; }
 };
 
+constexpr int kMaxBuckets = 12;  // SPD buckets of the bucket-bias form (spd_cap <= 10; Trainer default 8)
+
 struct DenseArgs {
   int64_t S, s_real;
   int H, dk, dv;
   int64_t ldq, ldv;
   const void *q, *k, *v, *o, *dout;
   const void* bias;   // A [S*S] or null
+  // bucket-bias form (the Trainer's dense epoch, model.cpp:395-423, 520-523):
+  // bias[r][c] = table[bucket[r][c]]; the backward reduces dbias per bucket
+  const uint8_t* bucket;  // [S*S] or null
+  const void* table;      // A [nb]
+  int nb;
+  void* dtable_part;      // A [gridDim.x][nb] (backward rows pass)
   const void* wmult;  // A [H*S*S] or null
   void *out, *lse, *dq, *dk_out, *dv_out;
   void* dbias;  // A [S*S] or null (backward)
@@ -118,12 +126,14 @@ template <typename T, int DH, int RPT>
 __global__ void __launch_bounds__(kBR / RPT) dense_fwd_kernel(DenseArgs a) {
   using A = typename Acc<T>::type;
   using M = DMath<A>;
-  __shared__ A Ks[kBC][DH], Vs[kBC][DH];
+  __shared__ A Ks[kBC][DH], Vs[kBC][DH], Tb[kMaxBuckets];
   const int h = blockIdx.y;
   const T* Q = static_cast<const T*>(a.q);
   const T* K = static_cast<const T*>(a.k);
   const T* V = static_cast<const T*>(a.v);
   const A* bias = static_cast<const A*>(a.bias);
+  const uint8_t* bk = a.bucket;
+  if (threadIdx.x < a.nb) Tb[threadIdx.x] = static_cast<const A*>(a.table)[threadIdx.x];
   const A* wm = static_cast<const A*>(a.wmult);
   T* O = static_cast<T*>(a.out);
   A* LSE = static_cast<A*>(a.lse);
@@ -160,6 +170,7 @@ __global__ void __launch_bounds__(kBR / RPT) dense_fwd_kernel(DenseArgs a) {
         for (int t = 0; t < DH; ++t) d += q[u][t] * Ks[c][t];
         A x = d * scale_l;
         if (bias && c < n) x += bias[r * a.S + c0 + c] * M::kL;
+        if (bk && c < n) x += Tb[bk[r * a.S + c0 + c]] * M::kL;
         s[c] = c < n ? x : M::ninf();
         mx = mx > s[c] ? mx : s[c];
       }
@@ -206,13 +217,17 @@ template <typename T, int DH, int RPT>
 __global__ void __launch_bounds__(kBR / RPT) dense_bwd_rows_kernel(DenseArgs a) {
   using A = typename Acc<T>::type;
   using M = DMath<A>;
-  __shared__ A Ks[kBC][DH], Vs[kBC][DH];
+  __shared__ A Ks[kBC][DH], Vs[kBC][DH], Tb[kMaxBuckets];
+  __shared__ A Dt[kBR / RPT][kMaxBuckets];  // per-thread table gradient (fixed-order reduction below)
   const T* Q = static_cast<const T*>(a.q);
   const T* K = static_cast<const T*>(a.k);
   const T* V = static_cast<const T*>(a.v);
   const T* O = static_cast<const T*>(a.o);
   const T* DO = static_cast<const T*>(a.dout);
   const A* bias = static_cast<const A*>(a.bias);
+  const uint8_t* bk = a.bucket;
+  if (threadIdx.x < a.nb) Tb[threadIdx.x] = static_cast<const A*>(a.table)[threadIdx.x];
+  for (int b = 0; b < kMaxBuckets; ++b) Dt[threadIdx.x][b] = 0;
   const A* wm = static_cast<const A*>(a.wmult);
   const A* LSE = static_cast<const A*>(a.lse);
   T* DQ = static_cast<T*>(a.dq);
@@ -257,9 +272,12 @@ __global__ void __launch_bounds__(kBR / RPT) dense_bwd_rows_kernel(DenseArgs a) 
           }
           A x = d * scale_l;
           if (bias) x += bias[r * a.S + c0 + c] * M::kL;
+          const int bkt = bk ? bk[r * a.S + c0 + c] : 0;
+          if (bk) x += Tb[bkt] * M::kL;
           const A p = M::ex(x - lse[u]);
           if (wm) dw *= wm[((int64_t)h * a.S + r) * a.S + c0 + c];
           const A ds = p * (dw - delta[u]);
+          if (bk) Dt[threadIdx.x][bkt] += ds;
 #pragma unroll
           for (int t = 0; t < DH; ++t) dq[u][t] += ds * Ks[c][t];
           if (DB) {
@@ -279,6 +297,24 @@ __global__ void __launch_bounds__(kBR / RPT) dense_bwd_rows_kernel(DenseArgs a) 
         if (t < a.dk) st_val(DQ + r * a.ldq + (int64_t)h * a.dk + t, real ? dq[u][t] * A(a.scale) : A(0));
     }
   }
+  if (bk) {  // this CTA's table gradient: threads summed in index order
+    __syncthreads();
+    if (threadIdx.x < a.nb) {
+      A g = 0;
+      for (int t = 0; t < (int)blockDim.x; ++t) g += Dt[t][threadIdx.x];
+      static_cast<A*>(a.dtable_part)[(int64_t)blockIdx.x * a.nb + threadIdx.x] = g;
+    }
+  }
+}
+
+// dtable[b] = sum over the rows pass's CTAs of their partials, in CTA order
+template <typename A>
+__global__ void dtable_reduce_kernel(const A* __restrict__ part, int nparts, int nb, A* __restrict__ out) {
+  const int b = threadIdx.x;
+  if (b >= nb) return;
+  A g = 0;
+  for (int x = 0; x < nparts; ++x) g += part[(int64_t)x * nb + b];
+  out[b] = g;
 }
 
 // ------------------------------------------------------------- bwd cols
@@ -286,8 +322,10 @@ template <typename T, int DH, int RPT>
 __global__ void __launch_bounds__(kBR / RPT) dense_bwd_cols_kernel(DenseArgs a) {
   using A = typename Acc<T>::type;
   using M = DMath<A>;
-  __shared__ A Qs[kBC][DH], Ds[kBC][DH], Ls[kBC], Dl[kBC];
+  __shared__ A Qs[kBC][DH], Ds[kBC][DH], Ls[kBC], Dl[kBC], Tb[kMaxBuckets];
   const int h = blockIdx.y;
+  const uint8_t* bk = a.bucket;
+  if (threadIdx.x < a.nb) Tb[threadIdx.x] = static_cast<const typename Acc<T>::type*>(a.table)[threadIdx.x];
   const T* Q = static_cast<const T*>(a.q);
   const T* K = static_cast<const T*>(a.k);
   const T* V = static_cast<const T*>(a.v);
@@ -352,6 +390,7 @@ __global__ void __launch_bounds__(kBR / RPT) dense_bwd_cols_kernel(DenseArgs a) 
         A x = d * scale_l;
         const int64_t r = i0 + i;
         if (bias) x += bias[r * a.S + c] * M::kL;
+        if (bk) x += Tb[bk[r * a.S + c]] * M::kL;
         const A p = M::ex(x - Ls[i]);
         A pw = p;
         if (wm) {
@@ -485,6 +524,66 @@ int gte_dense_attn_bwd(gte_ctx* ctx, int dtype, int64_t S, int64_t s_real, int H
   DCUDA(launch(dtype, 1, a, st));
   DCUDA(launch(dtype, 2, a, st));
   ctx_launch_counter(ctx) += 2;
+  return GTE_OK;
+}
+
+// Bucket-bias form: the Trainer's dense epoch (model.cpp:395-423, 520-523)
+// without an S x S float bias: bias[r][c] = table[buckets[r][c]] (uint8
+// buckets from gte_dense_buckets), dtable[b] = sum of dbias over bucket b
+// (fixed order: per-thread, per-CTA, then across CTAs). CUDA-core kernels for
+// every dtype.
+int gte_dense_attn_fwd_buckets(gte_ctx* ctx, int dtype, int64_t S, int64_t s_real, int H, int dk, int dv,
+                               const void* q, const void* k, int64_t ldq, const void* v, int64_t ldv,
+                               const uint8_t* buckets, const void* table, int64_t n_buckets, const void* wmult,
+                               void* out, void* lse) {
+  int rc = check_args(dtype, S, s_real, H, dk, dv, ldq, ldv);
+  if (rc) return rc;
+  if (!buckets || !table || n_buckets < 1 || n_buckets > kMaxBuckets)
+    return set_error(GTE_CONFIG, "dense_attention: bucket bias needs 1.." + std::to_string(kMaxBuckets) + " buckets");
+  if (S == 0) return GTE_OK;
+  DenseArgs a{};
+  a.S = S, a.s_real = s_real, a.H = H, a.dk = dk, a.dv = dv, a.ldq = ldq, a.ldv = ldv;
+  a.q = q, a.k = k, a.v = v, a.wmult = wmult, a.out = out, a.lse = lse;
+  a.bucket = buckets, a.table = table, a.nb = (int)n_buckets;
+  a.scale = 1.0 / std::sqrt((double)dk);
+  DCUDA(launch(dtype, 0, a, (cudaStream_t)ctx_stream(ctx)));
+  ctx_launch_counter(ctx) += 1;
+  return GTE_OK;
+}
+
+int gte_dense_attn_bwd_buckets(gte_ctx* ctx, int dtype, int64_t S, int64_t s_real, int H, int dk, int dv,
+                               const void* q, const void* k, int64_t ldq, const void* v, int64_t ldv, const void* out,
+                               const void* lse, const void* dout, const uint8_t* buckets, const void* table,
+                               int64_t n_buckets, const void* wmult, void* dq, void* dk_out, void* dv_out,
+                               void* dtable) {
+  int rc = check_args(dtype, S, s_real, H, dk, dv, ldq, ldv);
+  if (rc) return rc;
+  if (!buckets || !table || n_buckets < 1 || n_buckets > kMaxBuckets)
+    return set_error(GTE_CONFIG, "dense_attention: bucket bias needs 1.." + std::to_string(kMaxBuckets) + " buckets");
+  if (S == 0) return GTE_OK;
+  DenseArgs a{};
+  a.S = S, a.s_real = s_real, a.H = H, a.dk = dk, a.dv = dv, a.ldq = ldq, a.ldv = ldv;
+  a.q = q, a.k = k, a.v = v, a.o = out, a.dout = dout, a.wmult = wmult, a.lse = const_cast<void*>(lse);
+  a.dq = dq, a.dk_out = dk_out, a.dv_out = dv_out;
+  a.bucket = buckets, a.table = table, a.nb = (int)n_buckets;
+  a.scale = 1.0 / std::sqrt((double)dk);
+  cudaStream_t st = (cudaStream_t)ctx_stream(ctx);
+  const int parts = (int)((S + kBR - 1) / kBR);
+  const size_t as = dtype == GTE_F64 ? 8 : 4;
+  void* part = nullptr;
+  DCUDA(cudaMallocAsync(&part, as * (size_t)parts * n_buckets, st));
+  a.dtable_part = part;
+  DCUDA(launch(dtype, 1, a, st));
+  DCUDA(launch(dtype, 2, a, st));
+  if (dtype == GTE_F64)
+    dtable_reduce_kernel<double><<<1, 32, 0, st>>>(static_cast<double*>(part), parts, (int)n_buckets,
+                                                   static_cast<double*>(dtable));
+  else
+    dtable_reduce_kernel<float><<<1, 32, 0, st>>>(static_cast<float*>(part), parts, (int)n_buckets,
+                                                  static_cast<float*>(dtable));
+  DCUDA(cudaGetLastError());
+  DCUDA(cudaFreeAsync(part, st));
+  ctx_launch_counter(ctx) += 3;
   return GTE_OK;
 }
 

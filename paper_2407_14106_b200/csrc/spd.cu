@@ -154,6 +154,13 @@ struct BfsArgs {
   const int32_t* tgt_off = nullptr;  // mode 2: targets of source s: [tgt_off[s], tgt_off[s+1])
   const int32_t* tgt = nullptr;
   int32_t* tgt_dist = nullptr;
+  // mode 3: dense bucket rows (execution coordinates) of the Trainer's dense
+  // epoch: row r < s_real of out [S x S] from a BFS of original node inv[r]
+  const int64_t* inv = nullptr;      // [S] execution position -> original id
+  const int64_t* fwd = nullptr;      // [s_real] original id -> execution position
+  int64_t S = 0, s_real = 0, global = -1;
+  int32_t graph_n = 0;
+  uint8_t* rows_out = nullptr;
 };
 
 // MODE 0: ball sizes; 1: sorted (node, distance) rows; 2: distances of the targets (early exit)
@@ -166,7 +173,20 @@ __global__ void __launch_bounds__(kBfsThreads) bfs_kernel(BfsArgs a) {
   int32_t* q = a.queue + (int64_t)blockIdx.x * a.n;
   uint8_t* dd = a.dist + (int64_t)blockIdx.x * a.n;
   for (int s = blockIdx.x; s < a.nsrc; s += gridDim.x) {
-    const int32_t src = a.srcs ? a.srcs[s] : s;
+    int32_t src = a.srcs ? a.srcs[s] : s;
+    if (MODE == 3) {  // bucket row s: unreachable everywhere, then the BFS ball
+      const int64_t i = a.inv[s];
+      uint8_t* row = a.rows_out + (int64_t)s * a.S;
+      const uint8_t fill = i == a.global ? 1 : (uint8_t)(a.cap + 1);  // global token: bucket 1 to all
+      for (int64_t c = threadIdx.x; c < a.S; c += blockDim.x) row[c] = fill;
+      __syncthreads();
+      if (i == a.global || i >= a.graph_n) {
+        if (threadIdx.x == 0) row[s] = 0;
+        __syncthreads();
+        continue;
+      }
+      src = (int32_t)i;
+    }
     for (int w = threadIdx.x; w < words; w += blockDim.x) seen[w] = 0;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -211,7 +231,19 @@ __global__ void __launch_bounds__(kBfsThreads) bfs_kernel(BfsArgs a) {
       }
       __syncthreads();
     }
-    if (MODE == 0) {
+    if (MODE == 3) {  // scatter the ball into the row; the global token's column is bucket 1
+      uint8_t* row = a.rows_out + (int64_t)s * a.S;
+      for (int32_t x = threadIdx.x; x < s_next; x += blockDim.x) {
+        const int32_t v = q[x];
+        const int64_t c = a.fwd[v];
+        if (c < a.s_real) row[c] = dd[v];
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        if (a.global >= 0) row[a.fwd[a.global]] = 1;
+        row[s] = 0;
+      }
+    } else if (MODE == 0) {
       if (threadIdx.x == 0) a.count[s] = s_next;
     } else if (MODE == 1) {
       // emit the visited set in node order: per-thread word ranges, block scan of popcounts
@@ -269,7 +301,8 @@ cudaError_t run_bfs(int mode, const BfsArgs& base, cudaStream_t st) {
   };
   if (mode == 0) return go(bfs_kernel<0>);
   if (mode == 1) return go(bfs_kernel<1>);
-  return go(bfs_kernel<2>);
+  if (mode == 2) return go(bfs_kernel<2>);
+  return go(bfs_kernel<3>);
 }
 
 // table = capped balls of every source (mode 0 sizes -> scan -> mode 1 rows)
@@ -549,6 +582,37 @@ int gte_pattern_buckets_graph(gte_ctx* c, int64_t rows, int64_t nnz, const int32
   }
   SPCUDA(cudaStreamSynchronize(st));
   ctx_launch_counter(c) += 2;
+  return GTE_OK;
+}
+
+// Dense-epoch bucket matrix (model.cpp:395-423 with dense_pattern_exec):
+// out[r][c] for execution rows r < s_real and real columns c < s_real; pad
+// rows/columns are left unset (pad rows attend only themselves, unbiased).
+int gte_dense_buckets(gte_ctx* c, int64_t S, int64_t s_real, const int64_t* d_perm_forward,
+                      const int64_t* d_perm_inverse, int64_t global_index, int64_t graph_n, int64_t graph_nnz,
+                      const int32_t* d_graph_row_ptr, const int32_t* d_graph_cols, int64_t max_dist, uint8_t* d_out) {
+  if (max_dist < 0) return set_error(GTE_CONFIG, "spd_table: max_dist must be >= 0");
+  if (max_dist > 253) return set_error(GTE_CONFIG, "dense buckets: max_dist must be <= 253");
+  if (s_real < 0 || s_real > S || graph_n > s_real) return set_error(GTE_CONFIG, "dense buckets: bad sizes");
+  cudaStream_t st = static_cast<cudaStream_t>(ctx_stream(c));
+  UAdj u;
+  SPCUDA(build_uadj(st, (int32_t)graph_n, (int32_t)graph_nnz, d_graph_row_ptr, d_graph_cols, u));
+  BfsArgs a;
+  a.n = (int32_t)graph_n;
+  a.cap = (int32_t)max_dist;
+  a.off = u.off.p;
+  a.adj = u.adj.p;
+  a.nsrc = (int32_t)s_real;
+  a.inv = d_perm_inverse;
+  a.fwd = d_perm_forward;
+  a.S = S;
+  a.s_real = s_real;
+  a.global = global_index;
+  a.graph_n = (int32_t)graph_n;
+  a.rows_out = d_out;
+  if (s_real > 0) SPCUDA(run_bfs(3, a, st));
+  SPCUDA(cudaStreamSynchronize(st));
+  ctx_launch_counter(c) += 5;
   return GTE_OK;
 }
 

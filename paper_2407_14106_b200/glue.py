@@ -29,6 +29,7 @@ def _bind():
         L.gte_spd_destroy.argtypes = [VP]
         L.gte_spd_pairs.argtypes = [VP, I64, I64, VP, VP, I64, I64, VP, VP, VP]
         L.gte_pattern_buckets_graph.argtypes = [VP, I64, I64, VP, VP, VP, I64, I64, I64, VP, VP, I64, VP]
+        L.gte_dense_buckets.argtypes = [VP, I64, I64, VP, VP, I64, I64, I64, VP, VP, I64, VP]
         L._glue_bound = True
     return L
 
@@ -157,3 +158,21 @@ def pattern_buckets_graph(row_offsets, cols, perm_inverse, global_index: int, gr
                                             global_index, gro.numel() - 1, gm, gro.data_ptr(), gco.data_ptr(),
                                             max_dist, out.data_ptr()))
     return out[:m]
+
+
+def dense_buckets(S: int, s_real: int, perm_forward, perm_inverse, global_index: int, graph_row_offsets, graph_cols,
+                  max_dist: int, ctx: Context | None = None):
+    """Bucket matrix of the Trainer's dense epoch (model.cpp:407-423) in
+    execution coordinates: uint8 CUDA tensor [S, S], rows/columns < s_real set
+    (0 self, 1 global token, capped SPD else), one device BFS per row."""
+    ctx = ctx or Context.get(0)
+    import torch
+
+    dev = torch.device("cuda", ctx.device)
+    gro, gco, gm = _dev_csr(graph_row_offsets, graph_cols, dev)
+    fwd = torch.tensor(np.asarray(perm_forward, dtype=np.int64), device=dev)
+    inv = torch.tensor(np.asarray(perm_inverse, dtype=np.int64), device=dev)
+    out = torch.empty((S, S), dtype=torch.uint8, device=dev)
+    check(_bind().gte_dense_buckets(ctx.h, S, s_real, fwd.data_ptr(), inv.data_ptr(), global_index, gro.numel() - 1,
+                                    gm, gro.data_ptr(), gco.data_ptr(), max_dist, out.data_ptr()))
+    return out
