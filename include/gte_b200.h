@@ -49,6 +49,12 @@ const char* gte_version(void);
 /* ---- context: device, stream, workspaces, latched device errors ---- */
 int gte_ctx_create(int device, gte_ctx** out);
 int gte_ctx_destroy(gte_ctx* ctx);
+/* device memory for callers without the CUDA runtime (the C++ drop-in):
+ * stream-ordered on the context; gte_copy_d2h synchronises */
+int gte_dev_alloc(gte_ctx* ctx, int64_t bytes, void** out);
+int gte_dev_free(gte_ctx* ctx, void* p);
+int gte_copy_h2d(gte_ctx* ctx, void* dst, const void* src, int64_t bytes);
+int gte_copy_d2h(gte_ctx* ctx, void* dst, const void* src, int64_t bytes);
 int gte_ctx_set_stream(gte_ctx* ctx, void* cuda_stream);
 int gte_ctx_sync(gte_ctx* ctx);
 /* number of kernels this context launched so far (bench evidence) */
@@ -341,6 +347,7 @@ typedef struct gte_comm gte_comm;
 int gte_sp_create(gte_ctx* ctx, int64_t P, int64_t rows_per_worker, const int64_t* token_ids,
                   const int64_t* perm_forward, gte_sp** out);
 int gte_sp_destroy(gte_sp* sp);
+int gte_sp_shape(const gte_sp* sp, int64_t* P, int64_t* rows_per_worker, int64_t* total);
 int gte_sp_pack_seq(gte_ctx* ctx, const gte_sp* sp, int dtype, int64_t d, int64_t H, const void* shard, void* send);
 int gte_sp_unpack_head(gte_ctx* ctx, const gte_sp* sp, int dtype, int64_t d, int64_t H, const void* recv,
                        void* slice_exec);
@@ -362,6 +369,27 @@ int gte_comm_all_gather(gte_comm* comm, gte_ctx* ctx, const void* send, void* re
 /* variable all-to-all: per-peer byte offsets and counts (0 = no message) */
 int gte_comm_all_to_allv(gte_comm* comm, gte_ctx* ctx, const void* send, const int64_t* send_off,
                          const int64_t* send_bytes, void* recv, const int64_t* recv_off, const int64_t* recv_bytes);
+/* ---- the distributed layer as one object (SURVEY §8(b6) gte_sp_layer_fwd/bwd;
+ * reference run_distributed_layer / run_distributed_layer_backward,
+ * parallel.cpp:190-252, 271-332) ----
+ * Built on a gte_sp (token ids + cluster permutation) and a plan (pattern in
+ * execution coordinates, S_pad rows). comm == NULL: all P workers in this
+ * process (the reference's in-process exchange); otherwise this process is
+ * worker `rank` of a P-rank NCCL communicator. Shard arrays hold one device
+ * pointer per local worker ([rows x d] each; P of them, or 1 with comm).
+ * bias [E] and wmult [H x E] are in the accumulate type and replicated.
+ * The backward reuses the forward's head slices and returns dbias summed
+ * over workers in worker order (parallel.cpp:319). The ledger stays with the
+ * caller (pure arithmetic: 4Sd/P per worker, parallel.cpp:83-94). */
+typedef struct gte_sp_layer gte_sp_layer;
+int gte_sp_layer_create(gte_ctx* ctx, const gte_sp* sp, const gte_plan* plan, gte_comm* comm, int rank, int dtype,
+                        int64_t H, int64_t d, gte_sp_layer** out);
+int gte_sp_layer_fwd(gte_sp_layer* layer, const void* const* q, const void* const* k, const void* const* v,
+                     const void* bias, const void* wmult, void* const* out, int flags);
+int gte_sp_layer_bwd(gte_sp_layer* layer, const void* const* dout, const void* bias, const void* wmult,
+                     void* const* dq, void* const* dk, void* const* dv, void* dbias);
+int gte_sp_layer_destroy(gte_sp_layer* layer);
+
 /* ---- cluster-halo sequence parallelism ("Mode H") ----
  * Each GPU owns a contiguous range of rows (all heads) and runs the attention
  * kernels on a local plan over [own rows | halo rows]; the halo exchange moves

@@ -63,6 +63,53 @@ struct PlanHandle {
     ck(gte_plan_create_host(ctx(), pat.rows, pat.nnz(), ro.data(), pat.cols.empty() ? nullptr : pat.cols.data(), &p));
   }
   ~PlanHandle() { gte_plan_destroy(p); }
+  PlanHandle(const PlanHandle&) = delete;
+  PlanHandle& operator=(const PlanHandle&) = delete;
+};
+
+// Device plans of the last few patterns, keyed by content (rows, nnz and a
+// FNV-1a hash of offsets + columns): a Trainer calls the attention with the
+// same layout every step, and a plan (int32 CSR + CSC + execution plan) is
+// built once per layout instead of once per call.
+std::shared_ptr<PlanHandle> plan_for(const AttnPattern& pat) {
+  uint64_t h = 1469598103934665603ULL;
+  auto mix = [&](const std::vector<Index>& v) {
+    for (Index x : v) {
+      h ^= static_cast<uint64_t>(x);
+      h *= 1099511628211ULL;
+    }
+  };
+  mix(pat.row_offsets);
+  mix(pat.cols);
+  struct Entry {
+    uint64_t key;
+    Index rows, nnz;
+    std::shared_ptr<PlanHandle> plan;
+  };
+  static std::mutex mu;
+  static std::vector<Entry> cache;  // most recent last
+  std::lock_guard<std::mutex> lock(mu);
+  for (size_t i = 0; i < cache.size(); ++i)
+    if (cache[i].key == h && cache[i].rows == pat.rows && cache[i].nnz == pat.nnz()) {
+      Entry e = cache[i];
+      cache.erase(cache.begin() + static_cast<std::ptrdiff_t>(i));
+      cache.push_back(e);
+      return e.plan;
+    }
+  auto plan = std::make_shared<PlanHandle>(pat);
+  cache.push_back({h, pat.rows, pat.nnz(), plan});
+  if (cache.size() > 8) cache.erase(cache.begin());
+  return plan;
+}
+
+// device buffer through the library's C ABI (the bridge has no CUDA runtime)
+struct DevMem {
+  void* p = nullptr;
+  explicit DevMem(size_t bytes) { ck(gte_dev_alloc(ctx(), static_cast<int64_t>(bytes), &p)); }
+  DevMem(const void* host, size_t bytes) : DevMem(bytes) { ck(gte_copy_h2d(ctx(), p, host, static_cast<int64_t>(bytes))); }
+  ~DevMem() { gte_dev_free(ctx(), p); }
+  DevMem(const DevMem&) = delete;
+  DevMem& operator=(const DevMem&) = delete;
 };
 
 void check_shapes(const Matrix& q, const Matrix& k, const Matrix& v) {  // attention.cpp:12-18
@@ -178,9 +225,9 @@ AttnResult sparse_attention(const Matrix& q, const Matrix& k, const Matrix& v, c
     throw ConfigError("sparse_attention: weight_mult size mismatch");
   AttnResult res;
   res.output = Matrix(q.rows(), v.cols());
-  PlanHandle plan(pat);
+  auto plan = plan_for(pat);
   std::vector<Real> lse;
-  run_fwd(plan, 1, q.cols(), v.cols(), q.data(), k.data(), v.data(), opt(bias), opt(weight_mult), res.output.data(), lse,
+  run_fwd(*plan, 1, q.cols(), v.cols(), q.data(), k.data(), v.data(), opt(bias), opt(weight_mult), res.output.data(), lse,
           forbid_empty_rows ? GTE_FORBID_EMPTY_ROWS : 0);
   res.macs.score_macs = pat.nnz() * q.cols();
   res.macs.weight_macs = pat.nnz() * v.cols();
@@ -208,7 +255,8 @@ AttnGrads sparse_attention_backward(const Matrix& q, const Matrix& k, const Matr
   g.dk = Matrix(s, dk);
   g.dv = Matrix(s, dv);
   g.dbias.assign(static_cast<size_t>(pat.nnz()), 0.0);
-  PlanHandle plan(pat);
+  const auto planp = plan_for(pat);
+  const PlanHandle& plan = *planp;
   Matrix out(s, dv);
   std::vector<Real> lse;
   // softmax statistics from the same kernels (the reference recomputes them
@@ -609,40 +657,6 @@ void ledger_add(CommLedger* ledger, Index src, Index dst, std::int64_t elems, bo
   }
 }
 
-// Full token-indexed [S x d] matrix from worker shards (rows by token id).
-Matrix gather_full(const std::vector<Matrix>& shards, const std::vector<std::vector<Index>>& ids, Index total, Index d) {
-  Matrix full(total, d);
-  for (size_t w = 0; w < shards.size(); ++w)
-    for (size_t r = 0; r < ids[w].size(); ++r) {
-      auto src = shards[w].row(static_cast<Index>(r));
-      std::copy(src.begin(), src.end(), full.row(ids[w][r]).begin());
-    }
-  return full;
-}
-
-Matrix permute_rows(const Matrix& m, const Permutation& perm) {  // parallel.cpp:48-55
-  Matrix out(m.rows(), m.cols());
-  for (Index r = 0; r < m.rows(); ++r) {
-    auto src = m.row(perm.inverse[static_cast<size_t>(r)]);
-    std::copy(src.begin(), src.end(), out.row(r).begin());
-  }
-  return out;
-}
-
-std::vector<Matrix> scatter_unpermuted(const Matrix& full_p, const Permutation& perm,
-                                       const std::vector<std::vector<Index>>& ids, Index d) {
-  std::vector<Matrix> out;
-  for (const auto& tok : ids) {
-    Matrix m(static_cast<Index>(tok.size()), d);
-    for (size_t r = 0; r < tok.size(); ++r) {
-      auto src = full_p.row(perm.forward[static_cast<size_t>(tok[r])]);
-      std::copy(src.begin(), src.end(), m.row(static_cast<Index>(r)).begin());
-    }
-    out.push_back(std::move(m));
-  }
-  return out;
-}
-
 }  // namespace
 
 // parallel.cpp:115-147 (in-process exchange + element ledger)
@@ -693,8 +707,90 @@ std::vector<Matrix> all_to_all_head_to_seq(const std::vector<Matrix>& head_slice
   return out;
 }
 
-// parallel.cpp:190-252: exchange accounting as the reference; the attention
-// itself runs once over all H heads on the GPU (results are P-independent).
+namespace {
+
+// P in-process workers of the distributed layer on the device (gte_sp_layer
+// with the loopback exchange): shards uploaded once, the Ulysses all-to-alls,
+// the cluster permutation and the per-worker H/P heads all in libgte_b200.
+struct DeviceLayer {
+  Index P, rows, d;
+  std::shared_ptr<PlanHandle> plan;
+  gte_sp* sp = nullptr;
+  gte_sp_layer* L = nullptr;
+  std::vector<std::unique_ptr<DevMem>> in, out, dq, dk, dv;
+  std::unique_ptr<DevMem> bias_d, wm_d;
+
+  DeviceLayer(const std::vector<std::vector<Index>>& ids, const Permutation& perm, const AttnPattern& pattern,
+              Index num_heads, Index d_)
+      : P(static_cast<Index>(ids.size())), rows(static_cast<Index>(ids[0].size())), d(d_) {
+    plan = plan_for(pattern);
+    std::vector<int64_t> tok;
+    for (const auto& t : ids) tok.insert(tok.end(), t.begin(), t.end());
+    ck(gte_sp_create(ctx(), P, rows, tok.data(), perm.forward.data(), &sp));
+    ck(gte_sp_layer_create(ctx(), sp, plan->p, nullptr, 0, GTE_F64, num_heads, d, &L));
+  }
+  ~DeviceLayer() {
+    gte_sp_layer_destroy(L);
+    gte_sp_destroy(sp);
+  }
+  std::vector<void*> upload(const std::vector<Matrix>& mats) {
+    std::vector<void*> ptrs;
+    for (const Matrix& m : mats) {
+      in.push_back(std::make_unique<DevMem>(m.data(), sizeof(Real) * static_cast<size_t>(rows * d)));
+      ptrs.push_back(in.back()->p);
+    }
+    return ptrs;
+  }
+  std::vector<void*> make(std::vector<std::unique_ptr<DevMem>>& into) {
+    std::vector<void*> ptrs;
+    for (Index w = 0; w < P; ++w) {
+      into.push_back(std::make_unique<DevMem>(sizeof(Real) * static_cast<size_t>(rows * d)));
+      ptrs.push_back(into.back()->p);
+    }
+    return ptrs;
+  }
+  void put_bias(std::span<const Real> bias, std::span<const Real> wm) {
+    if (!bias.empty() && !bias_d) bias_d = std::make_unique<DevMem>(bias.data(), sizeof(Real) * bias.size());
+    if (!wm.empty() && !wm_d) wm_d = std::make_unique<DevMem>(wm.data(), sizeof(Real) * wm.size());
+  }
+  void forward(const std::vector<Matrix>& q, const std::vector<Matrix>& k, const std::vector<Matrix>& v,
+               std::span<const Real> bias, std::span<const Real> wm, int flags) {
+    put_bias(bias, wm);
+    const auto qp = upload(q), kp = upload(k), vp = upload(v);
+    const auto op = make(out);
+    ck(gte_sp_layer_fwd(L, qp.data(), kp.data(), vp.data(), bias_d ? bias_d->p : nullptr, wm_d ? wm_d->p : nullptr,
+                        op.data(), flags));
+    ck(gte_ctx_sync(ctx()));  // data-dependent errors (attention.cpp:20-22, 119-123)
+  }
+  void backward(const std::vector<Matrix>& up, std::span<const Real> bias, std::span<const Real> wm, Real* dbias) {
+    put_bias(bias, wm);
+    const auto upp = upload(up);
+    const auto a = make(dq), b = make(dk), c = make(dv);
+    DevMem db(sizeof(Real) * static_cast<size_t>(plan_nnz() + 1));
+    ck(gte_sp_layer_bwd(L, upp.data(), bias_d ? bias_d->p : nullptr, wm_d ? wm_d->p : nullptr, a.data(), b.data(),
+                        c.data(), db.p));
+    ck(gte_copy_d2h(ctx(), dbias, db.p, static_cast<int64_t>(sizeof(Real) * plan_nnz())));
+  }
+  int64_t plan_nnz() const {
+    int64_t nnz = 0;
+    gte_plan_shape(plan->p, nullptr, &nnz, nullptr, nullptr);
+    return nnz;
+  }
+  std::vector<Matrix> download(const std::vector<std::unique_ptr<DevMem>>& bufs, Index cols) {
+    std::vector<Matrix> res;
+    for (const auto& b : bufs) {
+      Matrix m(rows, cols);
+      ck(gte_copy_d2h(ctx(), m.data(), b->p, static_cast<int64_t>(sizeof(Real) * static_cast<size_t>(rows * cols))));
+      res.push_back(std::move(m));
+    }
+    return res;
+  }
+};
+
+}  // namespace
+
+// parallel.cpp:190-252: exchange accounting as the reference; the workers'
+// exchanges and heads run on the device (gte_sp_layer, loopback exchange).
 DistAttnResult run_distributed_layer(const std::vector<WorkerShard>& shards, const AttnPattern& pattern,
                                      const Permutation& perm, Index num_heads, std::span<const Real> bias,
                                      std::span<const Real> weight_mult, CommLedger& ledger) {
@@ -726,18 +822,13 @@ DistAttnResult run_distributed_layer(const std::vector<WorkerShard>& shards, con
   }
   if (!bias.empty())
     for (auto& e : ledger.workers) e.bias_exchange += static_cast<std::int64_t>(bias.size());
-  const Matrix qp = permute_rows(gather_full(qm, ids, total, d), perm);
-  const Matrix kp = permute_rows(gather_full(km, ids, total, d), perm);
-  const Matrix vp = permute_rows(gather_full(vm, ids, total, d), perm);
-  Matrix out_p(total, d);
-  PlanHandle plan(pattern);
-  std::vector<Real> lse;
-  run_fwd(plan, static_cast<int>(num_heads), hd, hd, qp.data(), kp.data(), vp.data(), opt(bias), opt(weight_mult),
-          out_p.data(), lse, 0);
+  // the layer on the device: Ulysses exchange + per-worker heads (gte_sp_layer)
+  DeviceLayer layer(ids, perm, pattern, num_heads, d);
+  layer.forward(qm, km, vm, bias, weight_mult, 0);
   DistAttnResult res;
   res.macs.score_macs = pattern.nnz() * hd * num_heads;
   res.macs.weight_macs = pattern.nnz() * hd * num_heads;
-  res.out_shards = scatter_unpermuted(out_p, perm, ids, d);
+  res.out_shards = layer.download(layer.out, d);
   // head -> seq exchange of O (parallel.cpp:250)
   for (Index src = 0; src < nw; ++src)
     for (Index dst = 0; dst < nw; ++dst) ledger_add(&ledger, src, dst, static_cast<std::int64_t>(total / nw) * (d / nw), false);
@@ -780,24 +871,18 @@ DistAttnGrads run_distributed_layer_backward(const std::vector<WorkerShard>& sha
   check_divisibility(d, num_heads, nw);
   const Index hd = d / num_heads;
   for (const std::vector<Matrix>* mats : std::initializer_list<const std::vector<Matrix>*>{&qm, &km, &vm, &upstream_shards}) validate_shards(*mats, ids);
-  const Matrix qp = permute_rows(gather_full(qm, ids, total, d), perm);
-  const Matrix kp = permute_rows(gather_full(km, ids, total, d), perm);
-  const Matrix vp = permute_rows(gather_full(vm, ids, total, d), perm);
-  const Matrix up = permute_rows(gather_full(upstream_shards, ids, total, d), perm);
-  PlanHandle plan(pattern);
-  Matrix out_p(total, d);
-  std::vector<Real> lse;
-  run_fwd(plan, static_cast<int>(num_heads), hd, hd, qp.data(), kp.data(), vp.data(), opt(bias), opt(weight_mult),
-          out_p.data(), lse, GTE_IGNORE_NONFINITE);
-  Matrix dq(total, d), dk(total, d), dv(total, d);
+  if (pattern.rows != total) throw ConfigError("run_distributed_layer: pattern/sequence mismatch");
+  if (perm.size() != total) throw ConfigError("run_distributed_layer: permutation size mismatch");
+  (void)hd;
+  DeviceLayer layer(ids, perm, pattern, num_heads, d);
+  layer.forward(qm, km, vm, bias, weight_mult, GTE_IGNORE_NONFINITE);  // no finiteness check in the backward
   std::vector<Real> db(static_cast<size_t>(pattern.nnz()) + 1, 0.0);
-  run_bwd(plan, static_cast<int>(num_heads), hd, hd, qp.data(), kp.data(), vp.data(), out_p.data(), lse, up.data(),
-          opt(bias), opt(weight_mult), dq.data(), dk.data(), dv.data(), db.data());
+  layer.backward(upstream_shards, bias, weight_mult, db.data());
   DistAttnGrads g;
   g.dbias.assign(db.begin(), db.begin() + pattern.nnz());
-  g.dq_sub = scatter_unpermuted(dq, perm, ids, d);
-  g.dk_sub = scatter_unpermuted(dk, perm, ids, d);
-  g.dv_sub = scatter_unpermuted(dv, perm, ids, d);
+  g.dq_sub = layer.download(layer.dq, d);
+  g.dk_sub = layer.download(layer.dk, d);
+  g.dv_sub = layer.download(layer.dv, d);
   return g;
 }
 

@@ -493,6 +493,29 @@ int gte_ctx_destroy(gte_ctx* c) {
   return GTE_OK;
 }
 
+// device memory for C/C++ callers without the CUDA runtime (the drop-in bridge)
+int gte_dev_alloc(gte_ctx* c, int64_t bytes, void** out) {
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaMalloc(out, bytes > 0 ? (size_t)bytes : 16));
+  return GTE_OK;
+}
+int gte_dev_free(gte_ctx* c, void* p) {
+  if (p) {
+    cudaStreamSynchronize(c->stream);
+    cudaFree(p);
+  }
+  return GTE_OK;
+}
+int gte_copy_h2d(gte_ctx* c, void* dst, const void* src, int64_t bytes) {
+  if (bytes > 0) CUDA_TRY(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyHostToDevice, c->stream));
+  return GTE_OK;
+}
+int gte_copy_d2h(gte_ctx* c, void* dst, const void* src, int64_t bytes) {
+  if (bytes > 0) CUDA_TRY(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return GTE_OK;
+}
+
 int gte_ctx_set_stream(gte_ctx* c, void* s) {
   c->stream = static_cast<cudaStream_t>(s);
   return GTE_OK;

@@ -296,6 +296,14 @@ int gte_sp_create(gte_ctx* ctx, int64_t P, int64_t rows_per_worker, const int64_
   return GTE_OK;
 }
 
+int gte_sp_shape(const gte_sp* s, int64_t* P, int64_t* rows_per_worker, int64_t* total) {
+  if (!s) return set_error(GTE_CONFIG, "all_to_all: null plan");
+  if (P) *P = s->P;
+  if (rows_per_worker) *rows_per_worker = s->rows;
+  if (total) *total = s->total;
+  return GTE_OK;
+}
+
 int gte_sp_destroy(gte_sp* s) {
   if (!s) return GTE_OK;
   cudaFree(s->d_tokens);
