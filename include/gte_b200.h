@@ -235,6 +235,25 @@ int gte_check_conditions(int64_t n, int64_t nnz, const int64_t* row_off, const i
 int gte_select_mode(const int32_t* flags, int64_t epoch, int64_t dense_period, int32_t* mode, int32_t* reason);
 int gte_partition_sequence(int64_t seq_len, int64_t num_workers, uint64_t seed, int64_t* ids, int64_t* padded);
 
+/* ---- ingestion formats (reference graph.cpp:68-109,
+ * 302-336, partition.cpp:458-493), parsed from memory (the drop-in hands over
+ * a std::istream's bytes); DataError with the reference's wording ----
+ * gte_parse_edge_list: "src dst" per line, '#' comments; num_nodes_hint < 0
+ *   = none (n = max id + 1, "empty graph" when no edge). Multi-threaded.
+ *   The CSR comes from gte_graph_from_edges_host (GPU sort + unique).
+ * gte_gtf1_decode: "GTF1", u64 N, u64 f, N*f float32; out = NULL reads the
+ *   shape only. gte_gtf1_encode: out = NULL returns the byte length.
+ * gte_parse_permutation: "old pos" per line; forward/inverse = NULL returns
+ *   the size only. */
+typedef struct gte_edges gte_edges;
+int gte_parse_edge_list(const char* text, int64_t len, int64_t num_nodes_hint, gte_edges** out);
+int gte_edges_info(const gte_edges* e, int64_t* num_nodes, int64_t* num_edges);
+int gte_edges_copy(const gte_edges* e, int64_t* src, int64_t* dst);
+int gte_edges_destroy(gte_edges* e);
+int gte_gtf1_decode(const void* bytes, int64_t len, int64_t* n, int64_t* f, float* out);
+int gte_gtf1_encode(int64_t n, int64_t f, const float* data, void* out, int64_t* len);
+int gte_parse_permutation(const char* text, int64_t len, int64_t* n, int64_t* forward, int64_t* inverse);
+
 /* ---- dense (all-pairs) attention, flash-style (reference attention.cpp:46-94,
  * 174-239; Trainer dense epochs model.cpp:395-405) ----
  * Rows r < s_real attend exactly the columns [0, s_real); pad rows r >= s_real

@@ -13,6 +13,9 @@
 // conformance kernels (dtype GTE_F64). Errors come back as gte_status codes
 // and are rethrown as the reference's exception types with its messages.
 #include <algorithm>
+#include <iterator>
+#include <istream>
+#include <ostream>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -151,6 +154,47 @@ Graph with_payload(Graph out, const Graph& src) {
 }  // namespace
 
 // ============================================================== graph.hpp
+
+namespace {
+std::string slurp(std::istream& in) { return std::string(std::istreambuf_iterator<char>(in), {}); }
+}  // namespace
+
+// graph.cpp:68-109: parsed in libgte_b200 (multi-threaded), CSR built on the GPU
+Graph load_edge_list(std::istream& in, std::optional<Index> num_nodes_hint) {
+  const std::string text = slurp(in);
+  gte_edges* e = nullptr;
+  ck(gte_parse_edge_list(text.data(), static_cast<int64_t>(text.size()), num_nodes_hint ? *num_nodes_hint : -1, &e));
+  int64_t n = 0, m = 0;
+  gte_edges_info(e, &n, &m);
+  std::vector<std::pair<Index, Index>> edges(static_cast<size_t>(m));
+  std::vector<int64_t> s(static_cast<size_t>(m)), d(static_cast<size_t>(m));
+  gte_edges_copy(e, s.data(), d.data());
+  gte_edges_destroy(e);
+  for (int64_t i = 0; i < m; ++i) edges[static_cast<size_t>(i)] = {s[static_cast<size_t>(i)], d[static_cast<size_t>(i)]};
+  return graph_from_edges(n, std::move(edges));
+}
+
+// graph.cpp:302-336 (GTF1)
+Matrix load_features_binary(std::istream& in) {
+  const std::string bytes = slurp(in);
+  int64_t n = 0, f = 0;
+  ck(gte_gtf1_decode(bytes.data(), static_cast<int64_t>(bytes.size()), &n, &f, nullptr));
+  std::vector<float> buf(static_cast<size_t>(n * f) + 1);
+  ck(gte_gtf1_decode(bytes.data(), static_cast<int64_t>(bytes.size()), &n, &f, buf.data()));
+  Matrix m(n, f);
+  for (int64_t i = 0; i < n * f; ++i) m.data()[i] = buf[static_cast<size_t>(i)];
+  return m;
+}
+
+void save_features_binary(std::ostream& out, const Matrix& m) {
+  std::vector<float> buf(static_cast<size_t>(m.rows() * m.cols()) + 1);
+  for (Index i = 0; i < m.rows() * m.cols(); ++i) buf[static_cast<size_t>(i)] = static_cast<float>(m.data()[i]);
+  int64_t len = 0;
+  gte_gtf1_encode(m.rows(), m.cols(), buf.data(), nullptr, &len);
+  std::string bytes(static_cast<size_t>(len), '\0');
+  ck(gte_gtf1_encode(m.rows(), m.cols(), buf.data(), bytes.data(), &len));
+  out.write(bytes.data(), static_cast<std::streamsize>(len));
+}
 
 // graph.cpp:49-66
 Graph graph_from_edges(Index num_nodes, std::vector<std::pair<Index, Index>> edges) {
@@ -340,7 +384,26 @@ bool Permutation::valid() const {  // partition.cpp:404-411
   return true;
 }
 
-// partition.cpp:413-433 (exact host reorder in libgte_b200)
+// partition.cpp:458-493
+void save_permutation(std::ostream& out, const Permutation& p) {
+  std::string text;
+  for (Index old = 0; old < p.size(); ++old)
+    text += std::to_string(old) + " " + std::to_string(p.forward[static_cast<size_t>(old)]) + "\n";
+  out << text;
+}
+
+Permutation load_permutation(std::istream& in) {
+  const std::string text = slurp(in);
+  int64_t n = 0;
+  ck(gte_parse_permutation(text.data(), static_cast<int64_t>(text.size()), &n, nullptr, nullptr));
+  Permutation p;
+  p.forward.assign(static_cast<size_t>(n), -1);
+  p.inverse.assign(static_cast<size_t>(n), -1);
+  ck(gte_parse_permutation(text.data(), static_cast<int64_t>(text.size()), &n, p.forward.data(), p.inverse.data()));
+  return p;
+}
+
+// partition.cpp:413-433 (device coarsening + host greedy passes in libgte_b200)
 Permutation reorder(const Graph& g, Index k, std::uint64_t seed) {
   Permutation p;
   p.forward.resize(static_cast<size_t>(g.num_nodes));
