@@ -235,6 +235,31 @@ int gte_check_conditions(int64_t n, int64_t nnz, const int64_t* row_off, const i
 int gte_select_mode(const int32_t* flags, int64_t epoch, int64_t dense_period, int32_t* mode, int32_t* reason);
 int gte_partition_sequence(int64_t seq_len, int64_t num_workers, uint64_t seed, int64_t* ids, int64_t* padded);
 
+/* ---- the transformer layer around the attention (reference
+ * Trainer forward/backward, model.cpp:533-595, 669-744; LayerNorm
+ * matrix.cpp:91-139, eps 1e-6; tanh GELU model.cpp:20-32) ----
+ * One pre-LN GPH block on the device over a plan (pattern in h's row order):
+ *   a = LN1(h); q,k,v = a W + b; attn = sparse attention (bias_vals [E]);
+ *   h += attn W_o + b_o; u = LN2(h) W_ff1 + b_ff1; h += gelu(u) W_ff2 + b_ff2
+ * Weights row-major [in x out] of dtype (X W); biases and LayerNorm scale /
+ * shift in the accumulate type. The forward keeps its activations for the
+ * backward, which ACCUMULATES parameter gradients (all in the accumulate
+ * type) into `grads`, adds into dh in place, and writes the attention's
+ * dbias_vals [E] (summed over heads). Projections are cuBLAS GEMMs; dropout
+ * off. */
+typedef struct gte_gph_params {
+  void *ln1_scale, *ln1_shift, *w_q, *b_q, *w_k, *b_k, *w_v, *b_v, *w_o, *b_o;
+  void *ln2_scale, *ln2_shift, *w_ff1, *b_ff1, *w_ff2, *b_ff2;
+} gte_gph_params;
+typedef struct gte_gph_layer gte_gph_layer;
+int gte_gph_layer_create(gte_ctx* ctx, const gte_plan* plan, int dtype, int heads, int hidden, int ffn,
+                         gte_gph_layer** out);
+int gte_gph_layer_set_params(gte_gph_layer* layer, const gte_gph_params* params);
+int gte_gph_layer_fwd(gte_gph_layer* layer, void* h, const void* bias_vals);
+int gte_gph_layer_bwd(gte_gph_layer* layer, void* dh, const void* bias_vals, const gte_gph_params* grads,
+                      void* dbias_vals);
+int gte_gph_layer_destroy(gte_gph_layer* layer);
+
 /* ---- ingestion formats (reference graph.cpp:68-109,
  * 302-336, partition.cpp:458-493), parsed from memory (the drop-in hands over
  * a std::istream's bytes); DataError with the reference's wording ----
