@@ -19,6 +19,7 @@
 // Random draws are libstdc++'s std::mt19937_64 / std::shuffle /
 // std::uniform_int_distribution, the reference's, in the same order.
 #include <algorithm>
+#include <climits>
 #include <cstdint>
 #include <cstdlib>
 #include <numeric>
@@ -27,12 +28,32 @@
 #include <stdexcept>
 #include <thread>
 #include <vector>
+#include <chrono>
+#include <cstdio>
+#include <mutex>
 
 #include "bisection.h"
 
 namespace gte_b200 {
 namespace part {
 namespace {
+
+// GTE_REORDER_TRACE=1: per-phase wall time on stderr (profiling only)
+struct Trace {
+  bool on = getenv("GTE_REORDER_TRACE") != nullptr;
+  std::mutex mu;
+  double t[8] = {};
+  static double now() { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); }
+  void add(int i, double dt) {
+    if (!on) return;
+    std::lock_guard<std::mutex> l(mu);
+    t[i] += dt;
+  }
+};
+Trace& trace() {
+  static Trace tr;
+  return tr;
+}
 
 constexpr int kFmPassLimit = 10;        // partition.cpp:17
 constexpr double kImbalanceTol = 0.05;  // partition.cpp:18
@@ -189,6 +210,70 @@ struct WeightClasses {
   }
 };
 
+// Best (key desc, node asc) over a range of weight classes: a tournament
+// tree whose leaf c holds the best entry pushed into class c since its last
+// refresh. A leaf entry that is still valid is its class's best valid node
+// (every node in the class queue is either older, hence no better than the
+// refreshed top, or a later push, hence no better than the leaf); an invalid
+// one is refreshed from the class queue. One range query per FM decision
+// instead of a scan over every feasible class.
+class ClassTournament {
+ public:
+  void reset(size_t n) {
+    size_ = 1;
+    while (size_ < n) size_ <<= 1;
+    key_.assign(2 * size_, kNoKey);
+    id_.assign(2 * size_, kNoId);
+  }
+  void offer(size_t c, int64_t key, int32_t id) {  // a push into class c
+    size_t x = size_ + c;
+    if (!better(key, id, key_[x], id_[x])) return;
+    key_[x] = key;
+    id_[x] = id;
+    for (x >>= 1; x; x >>= 1) pull(x);
+  }
+  void set(size_t c, int64_t key, int32_t id) {  // refreshed leaf
+    size_t x = size_ + c;
+    key_[x] = key;
+    id_[x] = id;
+    for (x >>= 1; x; x >>= 1) pull(x);
+  }
+  // class index of the best leaf in [lo, hi], or -1 when all are empty
+  long best(size_t lo, size_t hi, int64_t* key, int32_t* id) const {
+    long at = -1;
+    int64_t bk = kNoKey;
+    int32_t bi = kNoId;
+    auto take = [&](size_t x) {
+      // descend to the leaf that holds node x's winner
+      if (!better(key_[x], id_[x], bk, bi)) return;
+      while (x < size_) x = (key_[2 * x] == key_[x] && id_[2 * x] == id_[x]) ? 2 * x : 2 * x + 1;
+      at = (long)(x - size_);
+      bk = key_[x];
+      bi = id_[x];
+    };
+    for (size_t l = lo + size_, r = hi + size_ + 1; l < r; l >>= 1, r >>= 1) {
+      if (l & 1) take(l++);
+      if (r & 1) take(--r);
+    }
+    *key = bk;
+    *id = bi;
+    return bk == kNoKey && bi == kNoId ? -1 : at;
+  }
+
+ private:
+  static constexpr int64_t kNoKey = INT64_MIN;
+  static constexpr int32_t kNoId = INT32_MAX;
+  static bool better(int64_t k1, int32_t i1, int64_t k2, int32_t i2) { return k1 != k2 ? k1 > k2 : i1 < i2; }
+  void pull(size_t x) {
+    const size_t w = better(key_[2 * x], id_[2 * x], key_[2 * x + 1], id_[2 * x + 1]) ? 2 * x : 2 * x + 1;
+    key_[x] = key_[w];
+    id_[x] = id_[w];
+  }
+  size_t size_ = 1;
+  std::vector<int64_t> key_;
+  std::vector<int32_t> id_;
+};
+
 class FmRefiner {
  public:
   FmRefiner(const WGraph& g, std::vector<uint8_t>& side, int64_t allow)
@@ -201,17 +286,23 @@ class FmRefiner {
 
  private:
   MaxQueue& queue(int s, int c) { return queues_[s * cls_.w.size() + c]; }
+  void push(int s, int c, int64_t key, int32_t v) {
+    queue(s, c).push(key, v);
+    tour_[s].offer((size_t)c, key, v);
+  }
 
   bool one_pass() {
     load_[0] = load_[1] = 0;
     for (int64_t v = 0; v < g_.n; ++v) load_[side_[v]] += g_.vw[v];
     for (auto& q : queues_) q.clear();
+    tour_[0].reset(cls_.w.size());
+    tour_[1].reset(cls_.w.size());
     for (int64_t v = 0; v < g_.n; ++v) {
       int64_t s = 0;
       for (int64_t a = g_.xoff[v]; a < g_.xoff[v + 1]; ++a) s += side_[g_.nbr[a]] != side_[v] ? g_.wt[a] : -g_.wt[a];
       gain_[v] = s;
       locked_[v] = 0;
-      queue(side_[v], cls_.of[v]).push(s, (int32_t)v);
+      push(side_[v], cls_.of[v], s, (int32_t)v);
     }
     std::vector<int32_t> order;
     order.reserve(g_.n);
@@ -227,7 +318,7 @@ class FmRefiner {
         const int32_t x = g_.nbr[a];
         if (locked_[x]) continue;
         gain_[x] += side_[x] == side_[v] ? -2 * (int64_t)g_.wt[a] : 2 * (int64_t)g_.wt[a];
-        queue(side_[x], cls_.of[x]).push(gain_[x], x);
+        push(side_[x], cls_.of[x], gain_[x], x);
       }
       if (run > best) {
         best = run;
@@ -241,24 +332,49 @@ class FmRefiner {
     return best > 0;
   }
 
-  // best feasible unlocked node over both sides and all feasible classes
+  // best feasible unlocked node over both sides and all feasible classes:
+  // a move of weight w from side s is feasible iff -allow <= D_s - 2w <= allow
   int32_t pick() {
     int32_t who = -1;
     int64_t who_gain = 0;
+    const size_t nc = cls_.w.size();
     for (int s = 0; s < 2; ++s) {
       const int64_t d = load_[s] - load_[1 - s];
-      for (size_t c = 0; c < cls_.w.size(); ++c) {
-        const int64_t after = d - 2 * cls_.w[c];
-        if (after > allow_) continue;
-        if (after < -allow_) break;
+      // classes ascending by weight: D - 2w decreases; feasible = [lo, hi]
+      size_t lo = 0, hi = nc;
+      {
+        size_t a = 0, b = nc;  // first c with d - 2w <= allow
+        while (a < b) {
+          const size_t m = (a + b) / 2;
+          if (d - 2 * cls_.w[m] <= allow_) b = m; else a = m + 1;
+        }
+        lo = a;
+        a = lo, b = nc;  // first c with d - 2w < -allow
+        while (a < b) {
+          const size_t m = (a + b) / 2;
+          if (d - 2 * cls_.w[m] < -allow_) b = m; else a = m + 1;
+        }
+        hi = a;  // exclusive
+      }
+      if (lo >= hi) continue;
+      auto ok = [&](int64_t k, int32_t y) { return !locked_[y] && side_[y] == s && gain_[y] == k; };
+      for (;;) {
         int64_t key;
         int32_t x;
-        auto ok = [&](int64_t k, int32_t y) { return !locked_[y] && side_[y] == s && gain_[y] == k; };
-        if (!queue(s, (int)c).top(ok, &key, &x)) continue;
-        if (who < 0 || key > who_gain || (key == who_gain && x < who)) {
-          who = x;
-          who_gain = key;
+        const long c = tour_[s].best(lo, hi - 1, &key, &x);
+        if (c < 0) break;
+        if (ok(key, x)) {
+          if (who < 0 || key > who_gain || (key == who_gain && x < who)) {
+            who = x;
+            who_gain = key;
+          }
+          break;
         }
+        // stale leaf: refresh it from its class queue
+        int64_t tk;
+        int32_t tx;
+        if (queue(s, (int)c).top(ok, &tk, &tx)) tour_[s].set((size_t)c, tk, tx);
+        else tour_[s].set((size_t)c, INT64_MIN, INT32_MAX);
       }
     }
     return who;
@@ -278,6 +394,7 @@ class FmRefiner {
   std::vector<int64_t> gain_;
   std::vector<uint8_t> locked_;
   std::vector<MaxQueue> queues_;
+  ClassTournament tour_[2];
   int64_t load_[2] = {0, 0};
 };
 
@@ -331,10 +448,14 @@ std::vector<uint8_t> bisect_level(cudaStream_t st, const WGraph& g, std::mt19937
   std::vector<std::vector<int32_t>> maps;
   const WGraph* cur = &g;
   while (cur->n > kCoarseStop) {
+    double t0 = Trace::now();
     const std::vector<int32_t> mate = heavy_matching(*cur, rng);
+    double t1 = Trace::now();
     WGraph c;
     std::vector<int32_t> cmap;
     dev_contract(st, *cur, mate, c, cmap);
+    trace().add(0, t1 - t0);
+    trace().add(1, Trace::now() - t1);
     if (static_cast<double>(c.n) > kMinShrink * static_cast<double>(cur->n)) break;
     maps.push_back(std::move(cmap));
     coarse.push_back(std::move(c));
@@ -361,10 +482,16 @@ std::vector<uint8_t> bisect_level(cudaStream_t st, const WGraph& g, std::mt19937
     std::vector<uint8_t> f(fine.n);
     for (int64_t v = 0; v < fine.n; ++v) f[v] = side[maps[l][v]];
     side = std::move(f);
+    const double t0 = Trace::now();
     FmRefiner(fine, side, allowance_of(fine)).run();
+    trace().add(l == 0 ? 2 : 3, Trace::now() - t0);
   }
+  const double t0 = Trace::now();
   rebalance(g, side);
+  const double t1 = Trace::now();
   FmRefiner(g, side, 1).run();
+  trace().add(4, t1 - t0);
+  trace().add(5, Trace::now() - t1);
   return side;
 }
 
@@ -390,7 +517,9 @@ void split_into(const WGraph& g, const std::vector<int32_t>& ids, int64_t k, uin
   std::vector<uint8_t> side = bisect_level(w.st, g, rng);
   WGraph sub[2];
   std::vector<int32_t> local[2];
+  const double ts = Trace::now();
   dev_split(w.st, g, side, sub, local);
+  trace().add(6, Trace::now() - ts);
   std::vector<int32_t> sub_ids[2];
   for (int s = 0; s < 2; ++s) {
     sub_ids[s].resize(local[s].size());
@@ -430,7 +559,14 @@ void reorder_cluster(int64_t n, const int64_t* row_off, const int64_t* cols, int
   std::vector<int32_t> ids(n);
   std::iota(ids.begin(), ids.end(), 0);
   std::vector<int64_t> pid(n, 0);
+  const double t0 = part::Trace::now();
   part::split_into(g, ids, k, part::mix64(seed ^ part::kSaltRoot), 0, pid, device);
+  if (part::trace().on) {
+    const double* t = part::trace().t;
+    fprintf(stderr, "reorder trace: total %.2f s | match %.2f contract(dev) %.2f fm_finest %.2f fm_coarse %.2f "
+            "rebalance %.2f fm_final %.2f split(dev) %.2f (thread-summed)\n", part::Trace::now() - t0, t[0], t[1], t[2],
+            t[3], t[4], t[5], t[6]);
+  }
   // stable order by part (partition.cpp:423-431): counting sort
   std::vector<int64_t> start(k + 1, 0);
   for (int64_t v = 0; v < n; ++v) ++start[pid[v] + 1];
