@@ -142,17 +142,21 @@ class ClockSampler:
                 "samples": len(rows)}
 
 
+TIMED_KERNEL_SOURCES = ("attn_tile.cuh", "attn_piece.cuh", "attn_sparse.cuh", "common.cuh", "tile_launch.cuh",
+                        "tile_bf16.cu", "tile_f32.cu")
+
+
 def kernel_sources_sha():
-    """sha256 over the CUDA sources of the library (names + bytes, sorted):
+    """sha256 over the sources of the timed kernels (tile_fwd / tile_bwd_rows /
+    tile_bwd_cols: their code, dispatch, instantiation units and build flags):
     ties a committed ncu traffic capture to the kernels it measured."""
     import hashlib
 
     d = os.path.join(ROOT, "paper_2407_14106_b200", "csrc")
     h = hashlib.sha256()
-    for name in sorted(os.listdir(d)):
-        if name.endswith((".cu", ".cuh", ".cpp", ".h")):
-            h.update(name.encode())
-            h.update(open(os.path.join(d, name), "rb").read())
+    for name in TIMED_KERNEL_SOURCES:
+        h.update(name.encode())
+        h.update(open(os.path.join(d, name), "rb").read())
     return h.hexdigest()[:16]
 
 

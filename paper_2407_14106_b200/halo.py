@@ -245,45 +245,71 @@ class HaloAttention:
             self._all_send = self._send_counts
             self._all_recv = self._recv_counts
         self.cache = {}
+        self._bufs = {}
 
-    def _ext(self, r: RankHalo, own, zero_tail: bool = False):
-        """[own | halo] buffer. Tails that no exchange fills (Q, dO) are zeroed:
-        the kernels' padding slots may read any row of the local index space."""
+    def _ext(self, r: RankHalo, own, name: str, zero_tail: bool = False):
+        """[own | halo] buffer, persistent per (rank, tensor): allocated once,
+        own rows copied in each step. Tails that no exchange fills (Q, dO) are
+        zeroed once: the kernels' padding slots may read any row of the local
+        index space."""
         if r.n_ext == r.n_own:
             return own.contiguous()
-        t = own.new_empty((r.n_ext, self.d))
+        key = (r.rank, name)
+        t = self._bufs.get(key)
+        if t is None or t.dtype != own.dtype or t.device != own.device:
+            t = own.new_empty((r.n_ext, self.d))
+            if zero_tail:
+                t[r.n_own:].zero_()
+            self._bufs[key] = t
         t[: r.n_own].copy_(own)
-        if zero_tail:
-            t[r.n_own:].zero_()
         return t
 
-    def _halo_in(self, tensors: dict):
-        """Fill the halo tails of ext buffers {rank: ext} with the owners' rows."""
-        sends, recvs = {}, {}
-        for r in self.ranks:
-            ext = tensors[r.rank]
-            sends[r.rank] = self.ops.gather(ext, self.idx[r.rank], int(self.idx[r.rank].numel()))
-            recvs[r.rank] = ext[r.n_own:]
-        self.x.exchange(sends, recvs, self._all_send_counts(), self._all_recv_counts(), self.d)
+    def _halo_in_kv(self, kx: dict, vx: dict):
+        """Fill the halo tails of the K and V ext buffers with the owners' rows:
+        one all_to_allv of [K row | V row] pairs (2d wide) instead of two."""
+        import torch
 
-    def _halo_back(self, tensors: dict):
-        """Send the halo rows' partial sums to their owners and add them."""
         sends, recvs = {}, {}
         for r in self.ranks:
-            ext = tensors[r.rank]
-            sends[r.rank] = ext[r.n_own:]
             n = int(self.idx[r.rank].numel())
-            recvs[r.rank] = ext.new_empty((max(n, 1), self.d))
-        # reverse direction: what rank p received from q, it now sends back to q
-        self.x.exchange(sends, recvs, self._all_recv_counts(), self._all_send_counts(), self.d)
+            m = r.n_ext - r.n_own
+            if n:
+                sends[r.rank] = torch.cat([self.ops.gather(kx[r.rank], self.idx[r.rank], n),
+                                           self.ops.gather(vx[r.rank], self.idx[r.rank], n)], dim=1)
+            else:
+                sends[r.rank] = kx[r.rank].new_zeros((1, 2 * self.d))
+            recvs[r.rank] = kx[r.rank].new_empty((max(m, 1), 2 * self.d))
+        self.x.exchange(sends, recvs, self._all_send_counts(), self._all_recv_counts(), 2 * self.d)
         for r in self.ranks:
-            # one call per source peer, in rank order: rows are unique within
-            # a peer's block (no atomics) and the summation order is fixed
+            m = r.n_ext - r.n_own
+            if m:
+                kx[r.rank][r.n_own:].copy_(recvs[r.rank][:m, : self.d])
+                vx[r.rank][r.n_own:].copy_(recvs[r.rank][:m, self.d:])
+
+    def _halo_back_kv(self, gk: dict, gv: dict):
+        """Send the halo rows' dK | dV partial sums to their owners in one
+        all_to_allv and add them to the owners' rows, source by source in
+        rank order (unique rows per source: no atomics, fixed order)."""
+        import torch
+
+        sends, recvs = {}, {}
+        for r in self.ranks:
+            m = r.n_ext - r.n_own
+            n = int(self.idx[r.rank].numel())
+            if m:
+                sends[r.rank] = torch.cat([gk[r.rank][r.n_own:], gv[r.rank][r.n_own:]], dim=1)
+            else:
+                sends[r.rank] = gk[r.rank].new_zeros((1, 2 * self.d))
+            recvs[r.rank] = gk[r.rank].new_empty((max(n, 1), 2 * self.d))
+        self.x.exchange(sends, recvs, self._all_recv_counts(), self._all_send_counts(), 2 * self.d)
+        for r in self.ranks:
             off = 0
             idx, rv = self.idx[r.rank], recvs[r.rank]
             for n in self._send_counts[r.rank]:
                 if n:
-                    self.ops.scatter_add(tensors[r.rank], idx[off:off + n], rv[off:off + n], n)
+                    blk = rv[off:off + n]
+                    self.ops.scatter_add(gk[r.rank], idx[off:off + n], blk[:, : self.d].contiguous(), n)
+                    self.ops.scatter_add(gv[r.rank], idx[off:off + n], blk[:, self.d:].contiguous(), n)
                 off += n
 
     def _all_send_counts(self):
@@ -294,13 +320,12 @@ class HaloAttention:
 
     def forward(self, q: dict, k: dict, v: dict, bias=None):
         """bias: the global pattern's [E] (each rank uses its edges' slice)."""
-        kx = {r.rank: self._ext(r, k[r.rank]) for r in self.ranks}
-        vx = {r.rank: self._ext(r, v[r.rank]) for r in self.ranks}
-        self._halo_in(kx)
-        self._halo_in(vx)
+        kx = {r.rank: self._ext(r, k[r.rank], "k") for r in self.ranks}
+        vx = {r.rank: self._ext(r, v[r.rank], "v") for r in self.ranks}
+        self._halo_in_kv(kx, vx)
         out = {}
         for r in self.ranks:
-            qx = self._ext(r, q[r.rank], zero_tail=True)
+            qx = self._ext(r, q[r.rank], "q", zero_tail=True)
             b = None if bias is None else bias[r.e_lo:r.e_hi]
             o, lse = self.ops.attn_fwd(r.rank, qx, kx[r.rank], vx[r.rank], b)
             self.cache[r.rank] = (qx, kx[r.rank], vx[r.rank], o, lse, b)
@@ -312,10 +337,9 @@ class HaloAttention:
         gq, gk, gv, gb = {}, {}, {}, {}
         for r in self.ranks:
             qx, kx, vx, o, lse, b = self.cache[r.rank]
-            dox = self._ext(r, dout[r.rank], zero_tail=True)
+            dox = self._ext(r, dout[r.rank], "do", zero_tail=True)
             dq, dk, dv, db = self.ops.attn_bwd(r.rank, qx, kx, vx, o, lse, dox, b)
             gq[r.rank], gk[r.rank], gv[r.rank], gb[r.rank] = dq, dk, dv, db
-        self._halo_back(gk)
-        self._halo_back(gv)
+        self._halo_back_kv(gk, gv)
         return {r.rank: (gq[r.rank][: r.n_own], gk[r.rank][: r.n_own], gv[r.rank][: r.n_own],
                          gb[r.rank][: r.e_hi - r.e_lo]) for r in self.ranks}
