@@ -113,6 +113,41 @@ def oracle_multihead(orc, g: CSR, r, H, dh):
     return out, dq, dk, dv, db
 
 
+def check_sampled_rows(r, ro, co, rows, H, dh, dtype, what):
+    """All heads of sampled rows against a float64 numpy restatement of
+    attention.cpp:96-162 / 241-320: the output row, the dQ row and the
+    head-summed dbias of the row's edges (parallel.cpp:319). `r`: fp64 numpy
+    q, k, v, do, bias (the dtype-rounded device inputs) and out, dq, db."""
+    scale = 1.0 / np.sqrt(dh)
+    got_o, want_o, got_q, want_q, got_b, want_b = [], [], [], [], [], []
+    for i in rows:
+        e0, e1 = int(ro[i]), int(ro[i + 1])
+        if e1 == e0:
+            continue
+        cols = co[e0:e1]
+        b = r["bias"][e0:e1]
+        dbs = np.zeros(e1 - e0)
+        o_row = np.zeros(H * dh)
+        q_row = np.zeros(H * dh)
+        for h in range(H):
+            sl = slice(h * dh, (h + 1) * dh)
+            kc, vc = r["k"][cols, sl], r["v"][cols, sl]
+            sc = kc @ r["q"][i, sl] * scale + b
+            p = np.exp(sc - sc.max())
+            p /= p.sum()
+            o_row[sl] = p @ vc
+            dw = vc @ r["do"][i, sl]
+            ds = np.zeros_like(p) if e1 - e0 == 1 else p * (dw - p @ dw)
+            q_row[sl] = scale * (ds @ kc)
+            dbs += ds
+        got_o.append(r["out"][i]); want_o.append(o_row)
+        got_q.append(r["dq"][i]); want_q.append(q_row)
+        got_b.append(r["db"][e0:e1]); want_b.append(dbs)
+    assert_close(np.concatenate(got_o), np.concatenate(want_o), dtype, f"{what} sampled rows out")
+    assert_close(np.concatenate(got_q), np.concatenate(want_q), dtype, f"{what} sampled rows dq")
+    assert_close(np.concatenate(got_b), np.concatenate(want_b), dtype, f"{what} sampled rows dbias (all heads)")
+
+
 @pytest.fixture(scope="module")
 def c1_graph():
     s, t = c1_edges()
@@ -160,9 +195,9 @@ def test_c4_malnet_shape_global_token(cuda, orc, c4_graph, H, dh):
     to / attended by every node, E = 2.84M; GPH-large H = 32, dh = 24) at full
     size in f32: the degree-524,289 row and column go through the generic
     kernels' two-level sums (dh = 24) or the tile path's hub kernels (H = 8,
-    dh = 8, the GPH-slim geometry). Heads 0, H/2 and H-1 are checked against the fp64 oracle (the oracle runs
-    ~2.5 s per head); dbias, a sum over all 32 heads, only for finiteness
-    (its head-summed parity is covered at C1/C2 and by the hub tests)."""
+    dh = 8, the GPH-slim geometry). Heads 0, H/2 and H-1 against the fp64
+    oracle over the whole graph (~2.5 s per head); every head, incl. the
+    head-summed dbias, on 96 sampled rows and the global token's row."""
     import torch
 
     ro, co = c4_graph
@@ -187,7 +222,13 @@ def test_c4_malnet_shape_global_token(cuda, orc, c4_graph, H, dh):
         wq, wk, wv, _ = orc.sparse_bwd(qh, kh, vh, G, b64, None, doh)
         for got, w, nm in ((dq, wq, "dq"), (dk, wk, "dk"), (dv, wv, "dv")):
             assert_close(f(got), w, "f32", f"C4 head {h} {nm}")
-    assert torch.isfinite(db[:E]).all()
+    # every head, sampled rows incl. the global token (degree 524,289):
+    # output, dQ and the head-summed dbias of their edges
+    deg = np.diff(ro)
+    rows = np.r_[np.random.default_rng(1).choice(S, 96, replace=False), np.argmax(deg)]
+    fn = lambda t: t.double().cpu().numpy()  # noqa: E731
+    rr = dict(q=fn(q), k=fn(k), v=fn(v), do=fn(do), bias=b64, out=fn(out), dq=fn(dq), db=fn(db)[:E])
+    check_sampled_rows(rr, ro, co, rows, H, dh, "f32", f"C4 H={H}")
 
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
@@ -246,7 +287,11 @@ def test_c5_papers_shape_heads(cuda, orc, c5_graph, dtype):
         wq, wk, wv, _ = orc.sparse_bwd(qh, kh, vh, G, b64, None, doh)
         for got, w, nm in ((dq, wq, "dq"), (dk, wk, "dk"), (dv, wv, "dv")):
             assert_close(f(got), w, dtype, f"C5 head {h} {nm}")
-    assert torch.isfinite(db[:E]).all()
+    # every head, 256 sampled rows: output, dQ, head-summed dbias
+    rows = np.random.default_rng(2).choice(S, 256, replace=False)
+    fn = lambda t: t.double().cpu().numpy()  # noqa: E731
+    rr = dict(q=fn(q), k=fn(k), v=fn(v), do=fn(do), bias=b64, out=fn(out), dq=fn(dq), db=fn(db)[:E])
+    check_sampled_rows(rr, ro, co, rows, H, dh, dtype, "C5")
 
 
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
