@@ -225,6 +225,7 @@ int gte_tuner_state(const gte_tuner* st, double* avg_loss, int64_t* idx, double*
 int gte_tuner_history(const gte_tuner* st, int64_t* epochs, double* ldr, int64_t* n);
 int gte_tuner_set(gte_tuner* st, double avg_loss, int64_t idx, int32_t has_loss, int64_t n_hist,
                   const int64_t* epochs, const double* ldr);
+int gte_tuner_load(gte_tuner* st, int64_t n_thresholds, const double* thresholds, int64_t delta);
 int gte_tuner_destroy(gte_tuner* st);
 int gte_select_k(int64_t l2_bytes, int64_t hidden_dim, int64_t i, int64_t* out);
 int gte_select_db(int64_t n, const int64_t* db, const double* thr, int64_t* out);

@@ -574,29 +574,34 @@ TunerState make_tuner_state(Real beta_g, Index delta) {
   return st;
 }
 
-// The same controller as gte_tuner_update (csrc/host_api.cpp), applied to
-// the caller-owned TunerState (reformation.cpp:240-265).
+// reformation.cpp:240-265: the caller-owned TunerState goes through the
+// library's controller (gte_tuner_update) and comes back updated.
 void tuner_update(TunerState& state, Real loss, Real epoch_time_s, Index epoch) {
-  if (epoch_time_s <= 0.0) throw ConfigError("tuner_update: epoch_time must be positive");
-  if (!state.has_loss) {
-    state.avg_loss = loss;
-    state.has_loss = true;
-    state.ldr_history.emplace_back(epoch, 0.0);
-    return;
+  gte_tuner* t = nullptr;
+  ck(gte_tuner_create(0.5, 1, &t));
+  std::unique_ptr<gte_tuner, int (*)(gte_tuner*)> hold(t, gte_tuner_destroy);
+  std::vector<int64_t> ep;
+  std::vector<double> ldr;
+  for (const auto& [e, v] : state.ldr_history) {
+    ep.push_back(e);
+    ldr.push_back(v);
   }
-  if (!state.ldr_history.empty() && epoch != state.ldr_history.back().first + 1)
-    throw ConfigError("tuner_update: epochs must be consecutive");
-  const Real prev = state.avg_loss;
-  state.avg_loss = 0.9 * prev + 0.1 * loss;
-  const Real ldr = (state.avg_loss - prev) / epoch_time_s;
-  state.ldr_history.emplace_back(epoch, ldr);
-  const Index lag = static_cast<Index>(state.ldr_history.size()) - 1 - state.delta;
-  if (epoch >= state.delta && lag >= 0) {
-    if (ldr >= state.ldr_history[static_cast<size_t>(lag)].second)
-      state.idx = std::min(state.idx + 1, state.thresholds.size() - 1);
-    else if (state.idx > 0)
-      --state.idx;
-  }
+  ck(gte_tuner_set(t, state.avg_loss, static_cast<int64_t>(state.idx), state.has_loss ? 1 : 0,
+                   static_cast<int64_t>(ep.size()), ep.data(), ldr.data()));
+  ck(gte_tuner_load(t, static_cast<int64_t>(state.thresholds.size()), state.thresholds.data(), state.delta));
+  ck(gte_tuner_update(t, loss, epoch_time_s, epoch));
+  std::vector<double> thr(state.thresholds.size() + 1);
+  int64_t n_thr = 0, idx = 0, n_hist = 0;
+  int32_t has = 0;
+  gte_tuner_state(t, &state.avg_loss, &idx, thr.data(), &n_thr, &has);
+  state.idx = static_cast<size_t>(idx);
+  state.has_loss = has != 0;
+  gte_tuner_history(t, nullptr, nullptr, &n_hist);
+  ep.assign(static_cast<size_t>(n_hist), 0);
+  ldr.assign(static_cast<size_t>(n_hist), 0.0);
+  gte_tuner_history(t, ep.data(), ldr.data(), &n_hist);
+  state.ldr_history.clear();
+  for (int64_t i = 0; i < n_hist; ++i) state.ldr_history.emplace_back(ep[static_cast<size_t>(i)], ldr[static_cast<size_t>(i)]);
 }
 
 Index select_k(std::int64_t l2_bytes, Index hidden_dim, Index i) {

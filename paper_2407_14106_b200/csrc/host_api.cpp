@@ -104,6 +104,16 @@ int gte_tuner_set(gte_tuner* st, double avg_loss, int64_t idx, int32_t has_loss,
   return GTE_OK;
 }
 
+// thresholds and lag of a caller-held tuner state (the drop-in's TunerState)
+int gte_tuner_load(gte_tuner* st, int64_t n_thresholds, const double* thresholds, int64_t delta) {
+  if (n_thresholds < 1) return set_error(GTE_CONFIG, "tuner: empty threshold set");
+  if (delta < 1) return set_error(GTE_CONFIG, "tuner: delta must be >= 1");
+  st->thresholds.assign(thresholds, thresholds + n_thresholds);
+  st->delta = delta;
+  if (st->idx >= st->thresholds.size()) st->idx = st->thresholds.size() - 1;
+  return GTE_OK;
+}
+
 int gte_tuner_destroy(gte_tuner* st) {
   delete st;
   return GTE_OK;
