@@ -150,6 +150,60 @@ __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.a
 __device__ __forceinline__ void tc_before_sync() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_after_sync() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
+// MN-major canonical offset: k index (keys / queries, 128 of them), n index
+__device__ __forceinline__ uint32_t canon_mn(int kidx, int n) {
+  return (uint32_t)((n >> 3) * 2048 + (kidx >> 3) * 128 + (kidx & 7) * 16 + (n & 7) * 2);
+}
+
+__host__ __device__ constexpr uint32_t instr_desc_bmn(int M, int N) { return instr_desc(M, N) | (1u << 16); }
+
+// 16-byte global -> shared copy that bypasses registers; src_bytes = 0 writes
+// zeros (padding keys / columns)
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(gmem), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// Forward K / V block [c0, c0 + n) of head h: K as a K-major [128 x DKP] tile
+// (B of S = Q K^T), V as an MN-major [DVP x 128] tile (B of O = P V, keys =
+// the MMA's K): both layouts take 16-byte rows, so the vector path stages
+// them with cp.async (no registers, in flight while the previous block
+// computes). Odd head widths stage element-wise, synchronously.
+template <int DKP, int DVP>
+__device__ __forceinline__ void fwd_stage_kv(const TcArgs& a, int h, int64_t c0, int n, unsigned char* Kb,
+                                             unsigned char* Vb) {
+  constexpr int kT = 2 * kM;
+  const int tid = threadIdx.x;
+  if (a.vec) {
+    for (int x = tid; x < kN * (DKP / 8); x += kT) {
+      const int c = x / (DKP / 8), kk = (x % (DKP / 8)) * 8;
+      const bool ok = c < n && kk < a.dk;
+      cp_async16(Kb + canon(c, kk, DKP), ok ? a.k + (c0 + c) * a.ldq + (int64_t)h * a.dk + kk : a.k, ok ? 16 : 0);
+    }
+    for (int x = tid; x < kN * (DVP / 8); x += kT) {
+      const int c = x / (DVP / 8), t0 = (x % (DVP / 8)) * 8;
+      const bool ok = c < n && t0 < a.dv;
+      cp_async16(Vb + canon_mn(c, t0), ok ? a.v + (c0 + c) * a.ldv + (int64_t)h * a.dv + t0 : a.v, ok ? 16 : 0);
+    }
+    cp_async_commit();
+    return;
+  }
+  for (int x = tid; x < kN * DKP; x += kT) {
+    const int c = x / DKP, kk = x % DKP;
+    __nv_bfloat16 val = __float2bfloat16(0.f);
+    if (c < n && kk < a.dk) val = a.k[(c0 + c) * a.ldq + (int64_t)h * a.dk + kk];
+    *reinterpret_cast<__nv_bfloat16*>(Kb + canon(c, kk, DKP)) = val;
+  }
+  for (int x = tid; x < kN * DVP; x += kT) {
+    const int c = x / DVP, t = x % DVP;
+    __nv_bfloat16 val = __float2bfloat16(0.f);
+    if (c < n && t < a.dv) val = a.v[(c0 + c) * a.ldv + (int64_t)h * a.dv + t];
+    *reinterpret_cast<__nv_bfloat16*>(Vb + canon_mn(c, t)) = val;
+  }
+}
+
 // 8 warps per 128-row tile: warps w and w + 4 share TMEM lane quadrant w & 3
 // (rows 32 (w & 3) ..) and split the 128 key columns in halves; row maxima
 // and sums combine through shared memory; each half accumulates half of the
@@ -162,9 +216,9 @@ __global__ void __launch_bounds__(2 * kM, 3) dense_tc_fwd_kernel(TcArgs a) {
   constexpr int kHalfV = DVP / 2;
   extern __shared__ __align__(1024) unsigned char smem[];
   unsigned char* Qs = smem;                       // [128 x DKP]
-  unsigned char* Ks = Qs + kM * DKP * 2;          // [128 x DKP]
-  unsigned char* Vt = Ks + kN * DKP * 2;          // [DVP x 128]
-  unsigned char* Ps = Vt + DVP * kN * 2;          // [128 x 128]
+  unsigned char* Ks = Qs + kM * DKP * 2;          // 2 x [128 x DKP], double-buffered
+  unsigned char* Vm = Ks + 2 * kN * DKP * 2;      // 2 x [DVP x 128] MN-major
+  unsigned char* Ps = Vm + 2 * DVP * kN * 2;      // [128 x 128]
   float* red = reinterpret_cast<float*>(Ps + kM * kN * 2);  // [2][128] partial maxima / sums
   uint64_t* bar = reinterpret_cast<uint64_t*>(red + 2 * kM);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
@@ -197,9 +251,9 @@ __global__ void __launch_bounds__(2 * kM, 3) dense_tc_fwd_kernel(TcArgs a) {
   tc_after_sync();
   const uint32_t tmem = *tmem_slot;
   const uint32_t t_row = tmem + ((uint32_t)(quad * 32) << 16);
-  const uint32_t sQ = (uint32_t)__cvta_generic_to_shared(Qs), sK = (uint32_t)__cvta_generic_to_shared(Ks);
-  const uint32_t sV = (uint32_t)__cvta_generic_to_shared(Vt), sP = (uint32_t)__cvta_generic_to_shared(Ps);
-  constexpr uint32_t kIdS = instr_desc(kM, kN), kIdO = instr_desc(kM, DVP);
+  const uint32_t sQ = (uint32_t)__cvta_generic_to_shared(Qs), sK0 = (uint32_t)__cvta_generic_to_shared(Ks);
+  const uint32_t sV0 = (uint32_t)__cvta_generic_to_shared(Vm), sP = (uint32_t)__cvta_generic_to_shared(Ps);
+  constexpr uint32_t kIdS = instr_desc(kM, kN), kIdO = instr_desc_bmn(kM, DVP);
 
   float m = -INFINITY, l = 0.f, acc[kHalfV];
 #pragma unroll
@@ -208,43 +262,21 @@ __global__ void __launch_bounds__(2 * kM, 3) dense_tc_fwd_kernel(TcArgs a) {
   const bool real = row < a.s_real;
   const int cbase = half * kHalfN;
 
-  for (int64_t c0 = 0; c0 < a.s_real; c0 += kN) {
+  fwd_stage_kv<DKP, DVP>(a, h, 0, (int)(a.s_real < kN ? a.s_real : kN), Ks, Vm);
+  int buf = 0;
+  for (int64_t c0 = 0; c0 < a.s_real; c0 += kN, buf ^= 1) {
     const int n = (int)(a.s_real - c0 < kN ? a.s_real - c0 : kN);
-    if (a.vec) {
-      for (int x = tid; x < kN * (DKP / 8); x += kT) {
-        const int c = x / (DKP / 8), kk = (x % (DKP / 8)) * 8;
-        uint4 val = make_uint4(0, 0, 0, 0);
-        if (c < n && kk < a.dk)
-          val = __ldg(reinterpret_cast<const uint4*>(a.k + (c0 + c) * a.ldq + (int64_t)h * a.dk + kk));
-        *reinterpret_cast<uint4*>(Ks + canon(c, kk, DKP)) = val;
-      }
-      for (int x = tid; x < kN * (DVP / 8); x += kT) {
-        const int c = x / (DVP / 8), t0 = (x % (DVP / 8)) * 8;
-        uint4 val = make_uint4(0, 0, 0, 0);
-        if (c < n && t0 < a.dv)
-          val = __ldg(reinterpret_cast<const uint4*>(a.v + (c0 + c) * a.ldv + (int64_t)h * a.dv + t0));
-        const __nv_bfloat16* e8 = reinterpret_cast<const __nv_bfloat16*>(&val);
-#pragma unroll
-        for (int t = 0; t < 8; ++t) *reinterpret_cast<__nv_bfloat16*>(Vt + canon(t0 + t, c, kN)) = e8[t];
-      }
-    } else {
-      for (int x = tid; x < kN * DKP; x += kT) {
-        const int c = x / DKP, kk = x % DKP;
-        __nv_bfloat16 val = __float2bfloat16(0.f);
-        if (c < n && kk < a.dk) val = a.k[(c0 + c) * a.ldq + (int64_t)h * a.dk + kk];
-        *reinterpret_cast<__nv_bfloat16*>(Ks + canon(c, kk, DKP)) = val;
-      }
-      for (int x = tid; x < kN * DVP; x += kT) {
-        const int c = x / DVP, t = x % DVP;
-        __nv_bfloat16 val = __float2bfloat16(0.f);
-        if (c < n && t < a.dv) val = a.v[(c0 + c) * a.ldv + (int64_t)h * a.dv + t];
-        *reinterpret_cast<__nv_bfloat16*>(Vt + canon(t, c, kN)) = val;
-      }
-    }
+    const uint32_t sK = sK0 + (uint32_t)(buf * kN * DKP * 2), sV = sV0 + (uint32_t)(buf * DVP * kN * 2);
+    cp_async_wait0();  // this block's K / V (issued one block ahead)
     fence_async_smem();
     tc_before_sync();
     __syncthreads();
     tc_after_sync();
+    if (c0 + kN < a.s_real) {  // next block into the other buffer (its MMAs finished last block)
+      const int64_t c1 = c0 + kN;
+      fwd_stage_kv<DKP, DVP>(a, h, c1, (int)(a.s_real - c1 < kN ? a.s_real - c1 : kN), Ks + (buf ^ 1) * kN * DKP * 2,
+                             Vm + (buf ^ 1) * DVP * kN * 2);
+    }
     if (tid == 0) {
 #pragma unroll
       for (int kc = 0; kc < DKP / 16; ++kc)
@@ -317,7 +349,7 @@ __global__ void __launch_bounds__(2 * kM, 3) dense_tc_fwd_kernel(TcArgs a) {
     if (tid == 0) {
 #pragma unroll
       for (int kc = 0; kc < kN / 16; ++kc)
-        mma_bf16(tmem, smem_desc(sP + kc * 256, 128, kN * 16), smem_desc(sV + kc * 256, 128, kN * 16), kIdO, kc > 0);
+        mma_bf16(tmem, smem_desc(sP + kc * 256, 128, kN * 16), smem_desc(sV + kc * 256, 128, 2048), kIdO, kc > 0);
       mma_commit(bar);
     }
     mbar_wait(bar, phase);
@@ -364,8 +396,8 @@ __global__ void __launch_bounds__(2 * kM, 3) dense_tc_fwd_kernel(TcArgs a) {
 
 template <int DKP, int DVP>
 cudaError_t launch(const TcArgs& a, cudaStream_t st) {
-  const size_t smem = (size_t)kM * DKP * 2 + (size_t)kN * DKP * 2 + (size_t)DVP * kN * 2 + (size_t)kM * kN * 2 +
-                      2 * kM * sizeof(float) + 16;
+  const size_t smem = (size_t)kM * DKP * 2 + 2 * (size_t)kN * DKP * 2 + 2 * (size_t)DVP * kN * 2 +
+                      (size_t)kM * kN * 2 + 2 * kM * sizeof(float) + 16;
   dim3 grid((unsigned)((a.S + kM - 1) / kM), (unsigned)a.H);
   if (a.bias || a.wmult) {
     cudaError_t e = cudaFuncSetAttribute(dense_tc_fwd_kernel<DKP, DVP, true>,
@@ -404,12 +436,6 @@ cudaError_t launch_dv(const TcArgs& a, cudaStream_t st) {
 // staged a second time in the canonical MN-major layout (8 k-rows x 16 B of
 // n per core matrix; LBO = 128 B along k, SBO = 2048 B along n).
 
-// MN-major canonical offset: k index (keys / queries, 128 of them), n index
-__device__ __forceinline__ uint32_t canon_mn(int kidx, int n) {
-  return (uint32_t)((n >> 3) * 2048 + (kidx >> 3) * 128 + (kidx & 7) * 16 + (n & 7) * 2);
-}
-
-__host__ __device__ constexpr uint32_t instr_desc_bmn(int M, int N) { return instr_desc(M, N) | (1u << 16); }
 
 struct TcBwdArgs {
   int64_t S, s_real;
