@@ -496,6 +496,30 @@ __device__ __forceinline__ void stage_rows8(const __nv_bfloat16* g, int64_t ld, 
   }
 }
 
+// stage_rows8 through cp.async (no registers; completes at the caller's
+// cp_async_wait0): the backward kernels stage block j + 1 while block j
+// computes. Odd head widths fall back to the synchronous element-wise path.
+template <int WP>
+__device__ __forceinline__ void stage_rows8_async(const __nv_bfloat16* g, int64_t ld, int h, int W, int64_t r0, int n,
+                                                  unsigned char* kmaj, unsigned char* mnmaj, int vec) {
+  if (!vec) {
+    stage_rows8<WP>(g, ld, h, W, r0, n, kmaj, mnmaj, 0);
+    return;
+  }
+  for (int x = threadIdx.x; x < 128 * (WP / 8); x += kBT) {
+    const int r = x / (WP / 8), c = (x % (WP / 8)) * 8;
+    const bool ok = r < n && c < W;
+    const __nv_bfloat16* src = ok ? g + (r0 + r) * ld + (int64_t)h * W + c : g;
+    if (kmaj) cp_async16(kmaj + canon(r, c, WP), src, ok ? 16 : 0);
+    if (mnmaj) cp_async16(mnmaj + canon_mn(r, c), src, ok ? 16 : 0);
+  }
+}
+
+__device__ __forceinline__ void cp_async4z(void* smem, const void* gmem, int src_bytes) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(gmem), "r"(src_bytes) : "memory");
+}
+
 // columns [c0, c0 + NC) of this thread's TMEM lane -> v (NC multiple of 8)
 template <int NC>
 __device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, float (&v)[NC]) {
@@ -514,10 +538,12 @@ __global__ void __launch_bounds__(kBT, 2) dense_tc_dq_kernel(TcBwdArgs a) {
   extern __shared__ __align__(1024) unsigned char smem[];
   unsigned char* Qs = smem;                    // [128 x DKP] K-major (A of S)
   unsigned char* Ds = Qs + kM * DKP * 2;       // [128 x DVP] K-major (A of dP)
-  unsigned char* Ks = Ds + kM * DVP * 2;       // [128 keys x DKP] K-major (B of S)
-  unsigned char* Vs = Ks + kN * DKP * 2;       // [128 keys x DVP] K-major (B of dP)
-  unsigned char* Km = Vs + kN * DVP * 2;       // [DKP x 128 keys] MN-major (B of dQ)
-  unsigned char* dS = Km + DKP * kN * 2;       // [128 x 128] K-major (A of dQ)
+  // key-block operands, double-buffered: [K | V | Km] per buffer
+  constexpr int kKB = kN * DKP * 2 + kN * DVP * 2 + DKP * kN * 2;
+  unsigned char* KB = Ds + kM * DVP * 2;       // 2 x {K [128 keys x DKP] K-major (B of S),
+                                               //      V [128 keys x DVP] K-major (B of dP),
+                                               //      Km [DKP x 128 keys] MN-major (B of dQ)}
+  unsigned char* dS = KB + 2 * kKB;            // [128 x 128] K-major (A of dQ)
   uint64_t* bar = reinterpret_cast<uint64_t*>(dS + kM * kN * 2);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, quad = warp & 3, half = warp >> 2;
@@ -549,17 +575,26 @@ __global__ void __launch_bounds__(kBT, 2) dense_tc_dq_kernel(TcBwdArgs a) {
   tc_after_sync();
   const uint32_t tmem = *tmem_slot, t_row = tmem + ((uint32_t)(quad * 32) << 16);
   const uint32_t sQ = (uint32_t)__cvta_generic_to_shared(Qs), sD = (uint32_t)__cvta_generic_to_shared(Ds);
-  const uint32_t sK = (uint32_t)__cvta_generic_to_shared(Ks), sV = (uint32_t)__cvta_generic_to_shared(Vs);
-  const uint32_t sKm = (uint32_t)__cvta_generic_to_shared(Km), sS = (uint32_t)__cvta_generic_to_shared(dS);
+  const uint32_t sKB = (uint32_t)__cvta_generic_to_shared(KB), sS = (uint32_t)__cvta_generic_to_shared(dS);
+  auto stage_keys = [&](int64_t c, int b) {
+    const int nn = (int)(a.s_real - c < kN ? a.s_real - c : kN);
+    unsigned char* base = KB + b * kKB;
+    stage_rows8_async<DKP>(a.k, a.ldq, h, a.dk, c, nn, base, base + kN * DKP * 2 + kN * DVP * 2, a.vec);
+    stage_rows8_async<DVP>(a.v, a.ldv, h, a.dv, c, nn, base + kN * DKP * 2, nullptr, a.vec);
+    cp_async_commit();
+  };
   uint32_t phase = 0;
-  for (int64_t c0 = 0; c0 < a.s_real; c0 += kN) {
+  if (a.s_real > 0) stage_keys(0, 0);
+  int buf = 0;
+  for (int64_t c0 = 0; c0 < a.s_real; c0 += kN, buf ^= 1) {
     const int n = (int)(a.s_real - c0 < kN ? a.s_real - c0 : kN);
-    stage_rows8<DKP>(a.k, a.ldq, h, a.dk, c0, n, Ks, Km, a.vec);
-    stage_rows8<DVP>(a.v, a.ldv, h, a.dv, c0, n, Vs, nullptr, a.vec);
+    const uint32_t sK = sKB + (uint32_t)(buf * kKB), sV = sK + kN * DKP * 2, sKm = sV + kN * DVP * 2;
+    cp_async_wait0();  // this block's keys (issued one block ahead)
     fence_async_smem();
     tc_before_sync();
     __syncthreads();
     tc_after_sync();
+    if (c0 + kN < a.s_real) stage_keys(c0 + kN, buf ^ 1);  // the other buffer's MMAs completed last block
     if (tid == 0) {  // S = Q K^T
 #pragma unroll
       for (int kc = 0; kc < DKP / 16; ++kc)
@@ -651,15 +686,16 @@ __global__ void __launch_bounds__(kBT, 2) dense_tc_dkdv_kernel(TcBwdArgs a) {
   extern __shared__ __align__(1024) unsigned char smem[];
   unsigned char* Ks = smem;                    // [128 keys x DKP] K-major (A of S^T)
   unsigned char* Vs = Ks + kM * DKP * 2;       // [128 keys x DVP] K-major (A of dP^T)
-  unsigned char* Qk = Vs + kM * DVP * 2;       // [128 q x DKP] K-major (B of S^T)
-  unsigned char* Dk = Qk + kN * DKP * 2;       // [128 q x DVP] K-major (B of dP^T)
-  unsigned char* Qm = Dk + kN * DVP * 2;       // [DKP x 128 q] MN-major (B of dK)
-  unsigned char* Dm = Qm + DKP * kN * 2;       // [DVP x 128 q] MN-major (B of dV)
-  unsigned char* Pt = Dm + DVP * kN * 2;       // [128 keys x 128 q] K-major (A of dV)
+  // query-block operands, double-buffered: [Qk | Dk | Qm | Dm | lse | delta] per buffer
+  constexpr int kQB = (kN * DKP + kN * DVP + DKP * kN + DVP * kN) * 2 + 2 * kN * 4;
+  unsigned char* QB = Vs + kM * DVP * 2;       // 2 x {Qk [128 q x DKP] K-major (B of S^T),
+                                               //      Dk [128 q x DVP] K-major (B of dP^T),
+                                               //      Qm [DKP x 128 q] MN-major (B of dK),
+                                               //      Dm [DVP x 128 q] MN-major (B of dV),
+                                               //      lse [128], delta [128] of the query block}
+  unsigned char* Pt = QB + 2 * kQB;            // [128 keys x 128 q] K-major (A of dV)
   unsigned char* St = Pt + kM * kN * 2;        // [128 keys x 128 q] K-major (A of dK)
-  float* ls = reinterpret_cast<float*>(St + kM * kN * 2);  // [128] lse of the query block
-  float* dl = ls + kN;                                     // [128] delta of the query block
-  uint64_t* bar = reinterpret_cast<uint64_t*>(dl + kN);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(St + kM * kN * 2);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, quad = warp & 3, half = warp >> 2;
   const int rl = quad * 32 + lane, cb = half * kHN, h = blockIdx.y;
@@ -682,29 +718,38 @@ __global__ void __launch_bounds__(kBT, 2) dense_tc_dkdv_kernel(TcBwdArgs a) {
   tc_after_sync();
   const uint32_t tmem = *tmem_slot, t_row = tmem + ((uint32_t)(quad * 32) << 16);
   const uint32_t sK = (uint32_t)__cvta_generic_to_shared(Ks), sV = (uint32_t)__cvta_generic_to_shared(Vs);
-  const uint32_t sQk = (uint32_t)__cvta_generic_to_shared(Qk), sDk = (uint32_t)__cvta_generic_to_shared(Dk);
-  const uint32_t sQm = (uint32_t)__cvta_generic_to_shared(Qm), sDm = (uint32_t)__cvta_generic_to_shared(Dm);
+  const uint32_t sQB = (uint32_t)__cvta_generic_to_shared(QB);
   const uint32_t sPt = (uint32_t)__cvta_generic_to_shared(Pt), sSt = (uint32_t)__cvta_generic_to_shared(St);
   constexpr uint32_t kColV = 128, kColK = 192;  // dV, dK accumulators
-  uint32_t phase = 0;
-  for (int64_t q0 = 0; q0 < a.s_real; q0 += kN) {
-    const int n = (int)(a.s_real - q0 < kN ? a.s_real - q0 : kN);
-    stage_rows8<DKP>(a.q, a.ldq, h, a.dk, q0, n, Qk, Qm, a.vec);
-    stage_rows8<DVP>(a.dout, a.ldv, h, a.dv, q0, n, Dk, Dm, a.vec);
-    if (tid < kN) {  // lse, delta of the block's queries (thread t: query q0 + t)
-      float l_ = 0.f, d_ = 0.f;
-      if (tid < n) {
-        const int64_t qr = q0 + tid;
-        l_ = a.lse[qr * a.H + h];
-        d_ = a.delta[qr * a.H + h];  // dq kernel's dO . O
-      }
-      ls[tid] = l_;
-      dl[tid] = d_;
+  constexpr int oDk = kN * DKP * 2, oQm = oDk + kN * DVP * 2, oDm = oQm + DKP * kN * 2, oLs = oDm + DVP * kN * 2;
+  auto stage_queries = [&](int64_t q, int b) {
+    const int nn = (int)(a.s_real - q < kN ? a.s_real - q : kN);
+    unsigned char* base = QB + b * kQB;
+    stage_rows8_async<DKP>(a.q, a.ldq, h, a.dk, q, nn, base, base + oQm, a.vec);
+    stage_rows8_async<DVP>(a.dout, a.ldv, h, a.dv, q, nn, base + oDk, base + oDm, a.vec);
+    if (tid < kN) {  // lse, delta (the dq kernel's dO . O) of the block's queries; zeros past the end
+      const bool ok = tid < nn;
+      const int64_t qr = ok ? q + tid : 0;
+      float* lsb = reinterpret_cast<float*>(base + oLs);
+      cp_async4z(lsb + tid, a.lse + qr * a.H + h, ok ? 4 : 0);
+      cp_async4z(lsb + kN + tid, a.delta + qr * a.H + h, ok ? 4 : 0);
     }
+    cp_async_commit();
+  };
+  uint32_t phase = 0;
+  if (a.s_real > 0) stage_queries(0, 0);
+  int buf = 0;
+  for (int64_t q0 = 0; q0 < a.s_real; q0 += kN, buf ^= 1) {
+    const int n = (int)(a.s_real - q0 < kN ? a.s_real - q0 : kN);
+    const uint32_t sQk = sQB + (uint32_t)(buf * kQB), sDk = sQk + oDk, sQm = sQk + oQm, sDm = sQk + oDm;
+    const float* ls = reinterpret_cast<const float*>(QB + buf * kQB + oLs);
+    const float* dl = ls + kN;
+    cp_async_wait0();  // this block's queries (issued one block ahead)
     fence_async_smem();
     tc_before_sync();
     __syncthreads();
     tc_after_sync();
+    if (q0 + kN < a.s_real) stage_queries(q0 + kN, buf ^ 1);  // the other buffer's MMAs completed last block
     if (tid == 0) {  // S^T = K Q^T
 #pragma unroll
       for (int kc = 0; kc < DKP / 16; ++kc)
@@ -822,10 +867,11 @@ __global__ void __launch_bounds__(kBT, 2) dense_tc_dkdv_kernel(TcBwdArgs a) {
 
 template <int DKP, int DVP>
 cudaError_t launch_bwd(const TcBwdArgs& a, cudaStream_t st) {
-  const size_t s1 = (size_t)kM * (DKP + DVP) * 2 + (size_t)kN * (DKP + DVP) * 2 + (size_t)DKP * kN * 2 +
+  const size_t s1 = (size_t)kM * (DKP + DVP) * 2 + 2 * ((size_t)kN * (DKP + DVP) * 2 + (size_t)DKP * kN * 2) +
                     (size_t)kM * kN * 2 + 16;
-  const size_t s2 = (size_t)kM * (DKP + DVP) * 2 + (size_t)kN * (DKP + DVP) * 2 + (size_t)(DKP + DVP) * kN * 2 +
-                    2 * (size_t)kM * kN * 2 + 2 * kN * 4 + 16;
+  const size_t s2 = (size_t)kM * (DKP + DVP) * 2 +
+                    2 * ((size_t)kN * (DKP + DVP) * 2 + (size_t)(DKP + DVP) * kN * 2 + 2 * kN * 4) +
+                    2 * (size_t)kM * kN * 2 + 16;
   cudaError_t e = cudaFuncSetAttribute(dense_tc_dq_kernel<DKP, DVP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)s1);
   if (e != cudaSuccess) return e;
