@@ -140,6 +140,35 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// packed f32 pairs (FFMA2 / FADD2 / FMUL2 on sm_100)
+__device__ __forceinline__ uint64_t pk2(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void upk2(uint64_t r, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint32_t bf16x2(float lo, float hi) {
+  __nv_bfloat162 b2 = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&b2);
+}
+
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -287,6 +316,73 @@ __global__ void __launch_bounds__(2 * kM, 3) dense_tc_fwd_kernel(TcArgs a) {
     mbar_wait(bar, phase);
     phase ^= 1;
     tc_after_sync();
+    // Full blocks without bias / weights (all but the last key block when
+    // BW is off): no per-element masks, packed FFMA2 / FADD2 (the softmax
+    // passes are issue-bound; the masks were ~40 % of their instructions).
+    if (!BW && n == kN) {
+      float mx = -INFINITY;
+#pragma unroll
+      for (int q4 = 0; q4 < kHalfN / 16; ++q4) {
+        float v16[16];
+        tmem_ld16(t_row + cbase + q4 * 16, v16);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) mx = fmaxf(mx, v16[i]);
+      }
+      red[half * kM + rl] = mx * a.scale_l;
+      __syncthreads();
+      const float mn = fmaxf(m, fmaxf(red[rl], red[kM + rl]));
+      const float corr = ex2_approx(m - mn);
+      const uint64_t sc2 = pk2(a.scale_l, a.scale_l), nm2 = pk2(-mn, -mn);
+      uint64_t l2 = pk2(0.f, 0.f);
+#pragma unroll
+      for (int q4 = 0; q4 < kHalfN / 16; ++q4) {
+        float v16[16];
+        tmem_ld16(t_row + cbase + q4 * 16, v16);
+#pragma unroll
+        for (int c8 = 0; c8 < 2; ++c8) {
+          uint32_t w[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int j = c8 * 8 + 2 * i;
+            float x0, x1;
+            upk2(fma2(pk2(v16[j], v16[j + 1]), sc2, nm2), x0, x1);
+            const float p0 = ex2_approx(x0), p1 = ex2_approx(x1);
+            l2 = add2(l2, pk2(p0, p1));
+            w[i] = bf16x2(p0, p1);
+          }
+          *reinterpret_cast<uint4*>(Ps + canon(rl, cbase + q4 * 16 + c8 * 8, kN)) =
+              make_uint4(w[0], w[1], w[2], w[3]);
+        }
+      }
+      float la, lb;
+      upk2(l2, la, lb);
+      l = l * corr + (la + lb);
+      m = mn;
+      fence_async_smem();
+      tc_before_sync();
+      __syncthreads();
+      tc_after_sync();
+      if (tid == 0) {
+#pragma unroll
+        for (int kc = 0; kc < kN / 16; ++kc)
+          mma_bf16(tmem, smem_desc(sP + kc * 256, 128, kN * 16), smem_desc(sV + kc * 256, 128, 2048), kIdO, kc > 0);
+        mma_commit(bar);
+      }
+      mbar_wait(bar, phase);
+      phase ^= 1;
+      tc_after_sync();
+#pragma unroll
+      for (int c8 = 0; c8 < kHalfV / 8; ++c8) {
+        float v8[8];
+        tmem_ld8(t_row + half * kHalfV + c8 * 8, v8);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[c8 * 8 + i] = fmaf(acc[c8 * 8 + i], corr, v8[i]);
+      }
+      tc_before_sync();
+      __syncthreads();
+      tc_after_sync();
+      continue;
+    }
     // pass 1: this thread's half-row maximum, combined with the partner's
     float mx = -INFINITY;
 #pragma unroll
