@@ -680,6 +680,8 @@ __global__ void __launch_bounds__(kBT, 2) dense_tc_dq_kernel(TcBwdArgs a) {
     cp_async_commit();
   };
   uint32_t phase = 0;
+  const bool rows_full = r0 + kM <= a.s_real;  // CTA-uniform
+  const uint64_t sc2 = pk2(a.scale_l, a.scale_l), nl2 = pk2(-lse, -lse), nd2 = pk2(-delta, -delta);
   if (a.s_real > 0) stage_keys(0, 0);
   int buf = 0;
   for (int64_t c0 = 0; c0 < a.s_real; c0 += kN, buf ^= 1) {
@@ -702,10 +704,21 @@ __global__ void __launch_bounds__(kBT, 2) dense_tc_dq_kernel(TcBwdArgs a) {
     phase ^= 1;
     tc_after_sync();
     float p[kHN];
+    const bool fast = !a.bias && n == kN && rows_full;
 #pragma unroll
     for (int q4 = 0; q4 < kHN / 16; ++q4) {
       float v16[16];
       tmem_ld16(t_row + cb + q4 * 16, v16);
+      if (fast) {  // full block, every row real, no bias: no masks, packed scale-shift
+#pragma unroll
+        for (int i = 0; i < 16; i += 2) {
+          float x0, x1;
+          upk2(fma2(pk2(v16[i], v16[i + 1]), sc2, nl2), x0, x1);
+          p[q4 * 16 + i] = ex2_approx(x0);
+          p[q4 * 16 + i + 1] = ex2_approx(x1);
+        }
+        continue;
+      }
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         const int c = cb + q4 * 16 + i;
@@ -737,9 +750,9 @@ __global__ void __launch_bounds__(kBT, 2) dense_tc_dq_kernel(TcBwdArgs a) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int j = c8 * 8 + 2 * i, pc = q4 * 16 + j;
-          const float d0 = p[pc] * (v16[j] - delta), d1 = p[pc + 1] * (v16[j + 1] - delta);
-          __nv_bfloat162 b2 = __floats2bfloat162_rn(d0, d1);
-          w[i] = *reinterpret_cast<uint32_t*>(&b2);
+          float d0, d1;  // p (dP - delta), packed
+          upk2(mul2(pk2(p[pc], p[pc + 1]), add2(pk2(v16[j], v16[j + 1]), nd2)), d0, d1);
+          w[i] = bf16x2(d0, d1);
         }
         *reinterpret_cast<uint4*>(dS + canon(rl, cb + q4 * 16 + c8 * 8, kN)) = make_uint4(w[0], w[1], w[2], w[3]);
       }
@@ -833,6 +846,7 @@ __global__ void __launch_bounds__(kBT, 2) dense_tc_dkdv_kernel(TcBwdArgs a) {
     cp_async_commit();
   };
   uint32_t phase = 0;
+  const bool keys_full = k0 + kM <= a.s_real;  // CTA-uniform
   if (a.s_real > 0) stage_queries(0, 0);
   int buf = 0;
   for (int64_t q0 = 0; q0 < a.s_real; q0 += kN, buf ^= 1) {
@@ -857,16 +871,30 @@ __global__ void __launch_bounds__(kBT, 2) dense_tc_dkdv_kernel(TcBwdArgs a) {
     phase ^= 1;
     tc_after_sync();
     float p[kHN];
+    const bool fast = !a.bias && n == kN && keys_full;
 #pragma unroll
     for (int q4 = 0; q4 < kHN / 16; ++q4) {
       float v16[16];
       tmem_ld16(t_row + cb + q4 * 16, v16);
+      if (fast) {  // full block, every key real, no bias: no masks
+        const float4* l4 = reinterpret_cast<const float4*>(ls + cb + q4 * 16);
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int c = cb + q4 * 16 + i;
-        float x = fmaf(v16[i], a.scale_l, -ls[c]);
-        if (a.bias && real && c < n) x = fmaf(a.bias[(q0 + c) * a.S + key], 1.4426950408889634f, x);
-        p[q4 * 16 + i] = (real && c < n) ? ex2_approx(x) : 0.f;
+        for (int i4 = 0; i4 < 4; ++i4) {
+          const float4 lv = l4[i4];
+          const int i = 4 * i4;
+          p[q4 * 16 + i] = ex2_approx(fmaf(v16[i], a.scale_l, -lv.x));
+          p[q4 * 16 + i + 1] = ex2_approx(fmaf(v16[i + 1], a.scale_l, -lv.y));
+          p[q4 * 16 + i + 2] = ex2_approx(fmaf(v16[i + 2], a.scale_l, -lv.z));
+          p[q4 * 16 + i + 3] = ex2_approx(fmaf(v16[i + 3], a.scale_l, -lv.w));
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int c = cb + q4 * 16 + i;
+          float x = fmaf(v16[i], a.scale_l, -ls[c]);
+          if (a.bias && real && c < n) x = fmaf(a.bias[(q0 + c) * a.S + key], 1.4426950408889634f, x);
+          p[q4 * 16 + i] = (real && c < n) ? ex2_approx(x) : 0.f;
+        }
       }
 #pragma unroll
       for (int c8 = 0; c8 < 2; ++c8) {
@@ -903,9 +931,10 @@ __global__ void __launch_bounds__(kBT, 2) dense_tc_dkdv_kernel(TcBwdArgs a) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int j = c8 * 8 + 2 * i, pc = q4 * 16 + j, c = cb + pc;
-          const float d0 = p[pc] * (v16[j] - dl[c]), d1 = p[pc + 1] * (v16[j + 1] - dl[c + 1]);
-          __nv_bfloat162 b2 = __floats2bfloat162_rn(d0, d1);
-          w[i] = *reinterpret_cast<uint32_t*>(&b2);
+          const float2 dd = *reinterpret_cast<const float2*>(dl + c);
+          float d0, d1;  // p (dP - delta), packed
+          upk2(mul2(pk2(p[pc], p[pc + 1]), add2(pk2(v16[j], v16[j + 1]), pk2(-dd.x, -dd.y))), d0, d1);
+          w[i] = bf16x2(d0, d1);
         }
         *reinterpret_cast<uint4*>(St + canon(rl, cb + q4 * 16 + c8 * 8, kN)) = make_uint4(w[0], w[1], w[2], w[3]);
       }
