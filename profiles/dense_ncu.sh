@@ -16,7 +16,8 @@ o, lse = att.forward(q, k, v)
 att.backward(q, k, v, o, lse, up)
 torch.cuda.synchronize()
 PY
-timeout 900 ncu --set full --clock-control none -k regex:"dense_tc" -c 3 -o /tmp/prof_dense -f python /tmp/dense_one.py > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"dense_tc" -c 3 -o /tmp/prof_dense -f python /tmp/dense_one.py > /dev/null 2>&1
+ncu -i /tmp/prof_dense.ncu-rep --page source --csv --print-source sass > $O/ncu_source_dense_tc.csv 2>/dev/null; gzip -f $O/ncu_source_dense_tc.csv
 ncu -i /tmp/prof_dense.ncu-rep --page raw --csv > $O/ncu_raw_dense_tc.csv
 python - <<'PY'
 import csv
