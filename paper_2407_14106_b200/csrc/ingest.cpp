@@ -166,13 +166,19 @@ int gte_gtf1_decode(const void* bytes, int64_t len, int64_t* n, int64_t* f, floa
   uint64_t nn = 0, ff = 0;
   std::memcpy(&nn, b + 4, 8);
   std::memcpy(&ff, b + 12, 8);
+  // header values bounded by the payload before any product is formed (a
+  // corrupt header must not overflow n * f * 4)
+  const uint64_t payload = (uint64_t)(len - 20);
+  if (ff > payload / sizeof(float) && nn > 0) {
+    return set_error(GTE_DATA, "features binary: truncated at row 0");
+  }
+  const uint64_t row = ff * sizeof(float);
+  const uint64_t have = row > 0 ? payload / row : nn;
+  if (have < nn) return set_error(GTE_DATA, "features binary: truncated at row " + std::to_string(have));
   *n = (int64_t)nn;
   *f = (int64_t)ff;
-  const int64_t row = (int64_t)(ff * sizeof(float));
   if (!out) return GTE_OK;
-  const int64_t have = (len - 20) / (row > 0 ? row : 1);
-  if (row > 0 && have < (int64_t)nn) return set_error(GTE_DATA, "features binary: truncated at row " + std::to_string(have));
-  std::memcpy(out, b + 20, (size_t)(nn * ff * sizeof(float)));
+  std::memcpy(out, b + 20, (size_t)(nn * row));
   return GTE_OK;
 }
 

@@ -76,3 +76,14 @@ def test_permutation_text():
         ingest.parse_permutation("0 5\n1 0\n")
     with pytest.raises(DataError, match="permutation: invalid pair 0 1"):
         ingest.parse_permutation("0 0\n0 1\n")
+
+
+def test_gtf1_corrupt_header_does_not_overflow():
+    """A header whose N * f * 4 overflows (or exceeds the payload) is a
+    truncation error, not a huge allocation or an out-of-bounds copy."""
+    import struct
+
+    for n, f in ((2 ** 62, 2 ** 62), (1, 2 ** 62), (2 ** 60, 1), (3, 5)):
+        data = b"GTF1" + struct.pack("<QQ", n, f) + b"\0" * 16
+        with pytest.raises(DataError, match="truncated at row"):
+            ingest.decode_gtf1(data)
