@@ -256,6 +256,18 @@ def _read_cache(pattern, info):
         return None
 
 
+def gather_ceiling(dtype):
+    """Measured row-gather ceiling (requested GB/s) for the C3 pattern in
+    community order, from profiles/micro/gather_bw_b200.json."""
+    path = os.path.join(ROOT, "profiles", "micro", "gather_bw_b200.json")
+    try:
+        cap = json.load(open(path))[f"{dtype}_c3_community_order_best_gbs"]
+    except (OSError, KeyError, ValueError):
+        return {"gather_ceiling_gbs": None, "ceiling_source": "profiles/micro/gather_bw_b200.json missing"}
+    return {"gather_ceiling_gbs": cap, "ceiling_source": "measured on B200: profiles/micro/gather_bw.cu, "
+                                                         f"{dtype} rows, C3 pattern in community order, no math"}
+
+
 def cached_workload(pattern, info):
     """make_workload with an on-disk cache of this run (same inputs -> same
     pattern; the cache only saves the host reorder/layout on repeat runs)."""
@@ -634,14 +646,16 @@ def main():
                      "kernel": "tile_fwd + tile_bwd_rows + tile_bwd_cols (3 launches per step)",
                      "algorithmic_bytes_per_step": alg},
         "kernels_ms": {"fwd": float(np.mean(fwd_ms)), "bwd": float(np.mean(bwd_ms))},
-        # the bound the kernels actually meet (DESIGN.md §3/§9): bytes the three
-        # passes request from the memory system per step — every pair gathers a
-        # full K and V row (CSR passes) or Q and dO row + (lse, delta) (CSC pass)
-        # — against the L2 (LTS) throughput cap of the microarchitecture guide
-        # (~6300 B/clk full chip, measured on B300; assumed for B200)
+        # the memory-side quantity the kernels move: bytes the
+        # three passes request per step — every pair gathers a full K and V row
+        # (CSR passes) or Q and dO row + (lse, delta) (CSC pass) — against the
+        # row-gather ceiling measured on B200 for this pattern
+        # (profiles/micro/gather_bw.cu: the same 16-byte-per-lane row gathers
+        # in community order with no math); the gap is the kernels' per-pair
+        # instruction stream, not the memory system
         "l2_gather": {"requested_bytes_per_step": int(E) * (6 * H * DH * e + 8 * H),
                       "achieved_gbs": int(E) * (6 * H * DH * e + 8 * H) / (ms * 1e-3) / 1e9,
-                      "lts_cap_gbs": 6300 * 1.965, "peak_source": "assumed (B300_MICROARCH.md LTS cap)"},
+                      **gather_ceiling(args.dtype)},
         "e2e": {"value": world * S / e2e_s, "unit": "nodes/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e2e_s * 1e3},
         "gpu_launches": int(launches),
