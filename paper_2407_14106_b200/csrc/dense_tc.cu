@@ -21,6 +21,8 @@
 //
 // At head_dim 8 the tensor cores are far from the bound: 128 exps per row per
 // key block (MUFU) dominate, 2 MMAs per block do the 4*dh flops per pair.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -103,21 +105,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       : "memory");
 }
 
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
-  uint32_t r[32];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
-      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
-        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
-        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-}
-
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
   uint32_t r[8];
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
@@ -179,58 +166,100 @@ __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.a
 __device__ __forceinline__ void tc_before_sync() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_after_sync() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
-// MN-major canonical offset: k index (keys / queries, 128 of them), n index
-__device__ __forceinline__ uint32_t canon_mn(int kidx, int n) {
-  return (uint32_t)((n >> 3) * 2048 + (kidx >> 3) * 128 + (kidx & 7) * 16 + (n & 7) * 2);
-}
-
+// MN-major canonical no-swizzle layout (B operand with K = keys / queries):
+// element (k index kidx, n) at (n >> 3) * 2048 + (kidx >> 3) * 128 +
+// (kidx & 7) * 16 + (n & 7) * 2, descriptor (LBO 128, SBO 2048); tl() below
+// produces exactly these bytes.
 __host__ __device__ constexpr uint32_t instr_desc_bmn(int M, int N) { return instr_desc(M, N) | (1u << 16); }
 
-// 16-byte global -> shared copy that bypasses registers; src_bytes = 0 writes
-// zeros (padding keys / columns)
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
-  const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(gmem), "r"(src_bytes) : "memory");
+// ---- TMA-staged operand tiles ("chunk-major"): a 128-row tile of one head is
+// stored as dh/8 chunks of 2 KB, chunk c = columns [8c, 8c + 8) of the 128
+// rows at 16 B per row. One TMA box {8 elements, 128 rows} lands one chunk.
+// The same bytes are
+//   * the canonical K-major no-swizzle layout with rows as M/N and columns as
+//     K: core matrix (8 rows x 16 B) strides LBO = 2048 (along K), SBO = 128
+//     (along M/N) -> kdesc();
+//   * the canonical MN-major layout above with rows as K and columns as N
+//     -> mndesc().
+// So an operand the backward needs both ways (K for S = Q K^T and dQ = dS K;
+// Q and dO in the dK/dV kernel) is staged once.
+__device__ __forceinline__ uint32_t tl(int r, int kk) {
+  return (uint32_t)((kk >> 3) * 2048 + r * 16 + (kk & 7) * 2);
 }
+__device__ __forceinline__ uint64_t kdesc(uint32_t saddr, int kc) { return smem_desc(saddr + kc * 4096, 2048, 128); }
+__device__ __forceinline__ uint64_t mndesc(uint32_t saddr, int kc) { return smem_desc(saddr + kc * 256, 128, 2048); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(bar)),
+               "r"(bytes)
+               : "memory");
+}
+// box {8 columns, 128 rows} at (column x, row y) -> 2 KB of shared memory;
+// rows past the map's extent (s_real) arrive as zeros
+__device__ __forceinline__ void tma_chunk(void* dst, const CUtensorMap* tm, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          (uint32_t)__cvta_generic_to_shared(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"((uint32_t)__cvta_generic_to_shared(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_prefetch(const CUtensorMap* tm) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tm)) : "memory");
+}
+
+// Stage rows [r0, r0 + 128) of head h (W valid of WP columns) chunk-major:
+// vec -> one elected thread issues W/8 TMA boxes on `bar` (the caller waits
+// on it); otherwise every thread copies element-wise, zero-filling.
+template <int WP>
+__device__ __forceinline__ void stage_tl(const CUtensorMap* tm, const __nv_bfloat16* g, int64_t ld, int h, int W,
+                                         int64_t r0, int n, unsigned char* dst, uint64_t* bar, int vec, int nthreads) {
+  if (vec) {
+    if (threadIdx.x == 0) {
+      mbar_expect_tx(bar, (uint32_t)(W / 8) * 2048u);
+      for (int c = 0; c < W / 8; ++c) tma_chunk(dst + c * 2048, tm, h * W + c * 8, (int)r0, bar);
+    }
+    return;
+  }
+  for (int x = threadIdx.x; x < 128 * WP; x += nthreads) {
+    const int r = x % 128, c = x / 128;
+    const __nv_bfloat16 val = (r < n && c < W) ? g[(r0 + r) * ld + (int64_t)h * W + c] : __float2bfloat16(0.f);
+    *reinterpret_cast<__nv_bfloat16*>(dst + tl(r, c)) = val;
+  }
+}
+
+// zero the chunks [W/8, WP/8) of a chunk-major tile (TMA never writes them)
+template <int WP>
+__device__ __forceinline__ void zero_pad_chunks(unsigned char* dst, int W, int nthreads) {
+  const int c0 = W / 8;
+  for (int x = threadIdx.x + c0 * 128; x < (WP / 8) * 128; x += nthreads)
+    *reinterpret_cast<uint4*>(dst + x * 16) = make_uint4(0, 0, 0, 0);
+}
+
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-// Forward K / V block [c0, c0 + n) of head h: K as a K-major [128 x DKP] tile
-// (B of S = Q K^T), V as an MN-major [DVP x 128] tile (B of O = P V, keys =
-// the MMA's K): both layouts take 16-byte rows, so the vector path stages
-// them with cp.async (no registers, in flight while the previous block
-// computes). Odd head widths stage element-wise, synchronously.
+// Forward K / V block [c0, c0 + n) of head h, chunk-major: K is the K-major B
+// of S = Q K^T, V the MN-major B of O = P V (keys = the MMA's K). The vector
+// path is one elected thread issuing TMA boxes on `bar` (in flight while the
+// previous block computes); odd head widths stage element-wise, synchronously.
 template <int DKP, int DVP>
-__device__ __forceinline__ void fwd_stage_kv(const TcArgs& a, int h, int64_t c0, int n, unsigned char* Kb,
-                                             unsigned char* Vb) {
+__device__ __forceinline__ void fwd_stage_kv(const TcArgs& a, const CUtensorMap* tmK, const CUtensorMap* tmV, int h,
+                                             int64_t c0, int n, unsigned char* Kb, unsigned char* Vb, uint64_t* bar) {
   constexpr int kT = 2 * kM;
-  const int tid = threadIdx.x;
   if (a.vec) {
-    for (int x = tid; x < kN * (DKP / 8); x += kT) {
-      const int c = x / (DKP / 8), kk = (x % (DKP / 8)) * 8;
-      const bool ok = c < n && kk < a.dk;
-      cp_async16(Kb + canon(c, kk, DKP), ok ? a.k + (c0 + c) * a.ldq + (int64_t)h * a.dk + kk : a.k, ok ? 16 : 0);
+    if (threadIdx.x == 0) {
+      mbar_expect_tx(bar, (uint32_t)(a.dk / 8 + a.dv / 8) * 2048u);
+      for (int c = 0; c < a.dk / 8; ++c) tma_chunk(Kb + c * 2048, tmK, h * a.dk + c * 8, (int)c0, bar);
+      for (int c = 0; c < a.dv / 8; ++c) tma_chunk(Vb + c * 2048, tmV, h * a.dv + c * 8, (int)c0, bar);
     }
-    for (int x = tid; x < kN * (DVP / 8); x += kT) {
-      const int c = x / (DVP / 8), t0 = (x % (DVP / 8)) * 8;
-      const bool ok = c < n && t0 < a.dv;
-      cp_async16(Vb + canon_mn(c, t0), ok ? a.v + (c0 + c) * a.ldv + (int64_t)h * a.dv + t0 : a.v, ok ? 16 : 0);
-    }
-    cp_async_commit();
     return;
   }
-  for (int x = tid; x < kN * DKP; x += kT) {
-    const int c = x / DKP, kk = x % DKP;
-    __nv_bfloat16 val = __float2bfloat16(0.f);
-    if (c < n && kk < a.dk) val = a.k[(c0 + c) * a.ldq + (int64_t)h * a.dk + kk];
-    *reinterpret_cast<__nv_bfloat16*>(Kb + canon(c, kk, DKP)) = val;
-  }
-  for (int x = tid; x < kN * DVP; x += kT) {
-    const int c = x / DVP, t = x % DVP;
-    __nv_bfloat16 val = __float2bfloat16(0.f);
-    if (c < n && t < a.dv) val = a.v[(c0 + c) * a.ldv + (int64_t)h * a.dv + t];
-    *reinterpret_cast<__nv_bfloat16*>(Vb + canon_mn(c, t)) = val;
-  }
+  stage_tl<DKP>(tmK, a.k, a.ldq, h, a.dk, c0, n, Kb, bar, 0, kT);
+  stage_tl<DVP>(tmV, a.v, a.ldv, h, a.dv, c0, n, Vb, bar, 0, kT);
 }
 
 // 8 warps per 128-row tile: warps w and w + 4 share TMEM lane quadrant w & 3
@@ -241,18 +270,19 @@ __device__ __forceinline__ void fwd_stage_kv(const TcArgs& a, int h, int64_t c0,
 template <int DKP, int DVP, bool BW>  // BW: a bias or a weight_mult is present
 // dh <= 16: 4 CTAs per SM (64 registers, TMEM 4 x 128 columns; measured
 // -3.4 % vs 3 CTAs at S = 32,768 despite a small spill); wider heads keep 3
-__global__ void __launch_bounds__(2 * kM, (DKP <= 16 && DVP <= 16) ? 4 : 3) dense_tc_fwd_kernel(TcArgs a) {
+__global__ void __launch_bounds__(2 * kM, (DKP <= 16 && DVP <= 16) ? 4 : 3)
+    dense_tc_fwd_kernel(TcArgs a, const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV) {
   constexpr int kT = 2 * kM;     // threads
   constexpr int kHalfN = kN / 2; // key columns per thread
   constexpr int kHalfV = DVP / 2;
   extern __shared__ __align__(1024) unsigned char smem[];
-  unsigned char* Qs = smem;                       // [128 x DKP]
-  unsigned char* Ks = Qs + kM * DKP * 2;          // 2 x [128 x DKP], double-buffered
-  unsigned char* Vm = Ks + 2 * kN * DKP * 2;      // 2 x [DVP x 128] MN-major
+  unsigned char* Qs = smem;                       // [128 x DKP] chunk-major
+  unsigned char* Ks = Qs + kM * DKP * 2;          // 2 x [128 x DKP] chunk-major, double-buffered
+  unsigned char* Vm = Ks + 2 * kN * DKP * 2;      // 2 x [128 x DVP] chunk-major (= MN-major [DVP x 128])
   unsigned char* Ps = Vm + 2 * DVP * kN * 2;      // [128 x 128]
   float* red = reinterpret_cast<float*>(Ps + kM * kN * 2);  // [2][128] partial maxima / sums
-  uint64_t* bar = reinterpret_cast<uint64_t*>(red + 2 * kM);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(red + 2 * kM);  // [0] MMA commits, [1 + b] TMA of buffer b
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 3);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int quad = warp & 3, half = warp >> 2;
@@ -267,15 +297,25 @@ __global__ void __launch_bounds__(2 * kM, (DKP <= 16 && DVP <= 16) ? 4 : 3) dens
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)));
+    for (int b = 0; b < 3; ++b) mbar_init(bar + b);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (a.vec) {
+      tma_prefetch(&tmK);
+      tma_prefetch(&tmV);
+    }
   }
   for (int x = tid; x < kM * DKP; x += kT) {
-    const int r = x / DKP, kk = x % DKP;
+    const int r = x % kM, kk = x / kM;
     const int64_t gr = r0 + r;
     __nv_bfloat16 val = __float2bfloat16(0.f);
     if (gr < a.s_real && kk < a.dk) val = a.q[gr * a.ldq + (int64_t)h * a.dk + kk];
-    *reinterpret_cast<__nv_bfloat16*>(Qs + canon(r, kk, DKP)) = val;
+    *reinterpret_cast<__nv_bfloat16*>(Qs + tl(r, kk)) = val;
+  }
+  if (a.vec) {  // the pad chunks TMA never writes
+    for (int b = 0; b < 2; ++b) {
+      zero_pad_chunks<DKP>(Ks + b * kN * DKP * 2, a.dk, kT);
+      zero_pad_chunks<DVP>(Vm + b * DVP * kN * 2, a.dv, kT);
+    }
   }
   tc_before_sync();
   __syncthreads();
@@ -293,26 +333,25 @@ __global__ void __launch_bounds__(2 * kM, (DKP <= 16 && DVP <= 16) ? 4 : 3) dens
   const bool real = row < a.s_real;
   const int cbase = half * kHalfN;
 
-  fwd_stage_kv<DKP, DVP>(a, h, 0, (int)(a.s_real < kN ? a.s_real : kN), Ks, Vm);
+  if (a.s_real > 0) fwd_stage_kv<DKP, DVP>(a, &tmK, &tmV, h, 0, (int)(a.s_real < kN ? a.s_real : kN), Ks, Vm, bar + 1);
   int buf = 0;
-  for (int64_t c0 = 0; c0 < a.s_real; c0 += kN, buf ^= 1) {
+  uint32_t blk = 0;
+  for (int64_t c0 = 0; c0 < a.s_real; c0 += kN, buf ^= 1, ++blk) {
     const int n = (int)(a.s_real - c0 < kN ? a.s_real - c0 : kN);
     const uint32_t sK = sK0 + (uint32_t)(buf * kN * DKP * 2), sV = sV0 + (uint32_t)(buf * DVP * kN * 2);
-    cp_async_wait0();  // this block's K / V (issued one block ahead)
+    if (a.vec) mbar_wait(bar + 1 + buf, (blk >> 1) & 1);  // this block's K / V (issued one block ahead)
     fence_async_smem();
     tc_before_sync();
     __syncthreads();
     tc_after_sync();
     if (c0 + kN < a.s_real) {  // next block into the other buffer (its MMAs finished last block)
       const int64_t c1 = c0 + kN;
-      fwd_stage_kv<DKP, DVP>(a, h, c1, (int)(a.s_real - c1 < kN ? a.s_real - c1 : kN), Ks + (buf ^ 1) * kN * DKP * 2,
-                             Vm + (buf ^ 1) * DVP * kN * 2);
+      fwd_stage_kv<DKP, DVP>(a, &tmK, &tmV, h, c1, (int)(a.s_real - c1 < kN ? a.s_real - c1 : kN),
+                             Ks + (buf ^ 1) * kN * DKP * 2, Vm + (buf ^ 1) * DVP * kN * 2, bar + 1 + (buf ^ 1));
     }
     if (tid == 0) {
 #pragma unroll
-      for (int kc = 0; kc < DKP / 16; ++kc)
-        mma_bf16(tmem, smem_desc(sQ + kc * 256, 128, DKP * 16), smem_desc(sK + kc * 256, 128, DKP * 16), kIdS,
-                 kc > 0);
+      for (int kc = 0; kc < DKP / 16; ++kc) mma_bf16(tmem, kdesc(sQ, kc), kdesc(sK, kc), kIdS, kc > 0);
       mma_commit(bar);
     }
     mbar_wait(bar, phase);
@@ -492,21 +531,45 @@ __global__ void __launch_bounds__(2 * kM, (DKP <= 16 && DVP <= 16) ? 4 : 3) dens
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
 }
 
+// Tensor map of a [rows x cols] bf16 matrix with row stride ld (elements) and
+// a {8 columns, 128 rows} box; rows past `rows` read as zeros.
+bool encode_rows_map(CUtensorMap* m, const void* base, int64_t cols, int64_t rows, int64_t ld) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
+  if (!encode) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)(rows > 0 ? rows : 1)};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  const cuuint32_t box[2] = {8, 128}, estr[2] = {1, 1};
+  return encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int DKP, int DVP>
 cudaError_t launch(const TcArgs& a, cudaStream_t st) {
   const size_t smem = (size_t)kM * DKP * 2 + 2 * (size_t)kN * DKP * 2 + 2 * (size_t)DVP * kN * 2 +
-                      (size_t)kM * kN * 2 + 2 * kM * sizeof(float) + 16;
+                      (size_t)kM * kN * 2 + 2 * kM * sizeof(float) + 32;
   dim3 grid((unsigned)((a.S + kM - 1) / kM), (unsigned)a.H);
+  CUtensorMap tk{}, tv{};
+  if (a.vec && !(encode_rows_map(&tk, a.k, (int64_t)a.H * a.dk, a.s_real, a.ldq) &&
+                 encode_rows_map(&tv, a.v, (int64_t)a.H * a.dv, a.s_real, a.ldv)))
+    return cudaErrorInvalidValue;
   if (a.bias || a.wmult) {
     cudaError_t e = cudaFuncSetAttribute(dense_tc_fwd_kernel<DKP, DVP, true>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    dense_tc_fwd_kernel<DKP, DVP, true><<<grid, 2 * kM, smem, st>>>(a);
+    dense_tc_fwd_kernel<DKP, DVP, true><<<grid, 2 * kM, smem, st>>>(a, tk, tv);
   } else {
     cudaError_t e = cudaFuncSetAttribute(dense_tc_fwd_kernel<DKP, DVP, false>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    dense_tc_fwd_kernel<DKP, DVP, false><<<grid, 2 * kM, smem, st>>>(a);
+    dense_tc_fwd_kernel<DKP, DVP, false><<<grid, 2 * kM, smem, st>>>(a, tk, tv);
   }
   return cudaGetLastError();
 }
@@ -550,66 +613,30 @@ struct TcBwdArgs {
 
 __device__ __forceinline__ __nv_bfloat16 bz() { return __float2bfloat16(0.f); }
 
-// stage rows [r0, r0+n) of a [S x (H*W)] bf16 tensor, head h, W valid of WP
-// columns, as a K-major [128 x WP] tile and (optionally) an MN-major
-// [WP x 128] tile (row index = k)
-template <int WP>
-__device__ __forceinline__ void stage_rows(const __nv_bfloat16* g, int64_t ld, int h, int W, int64_t r0, int n,
-                                           unsigned char* kmaj, unsigned char* mnmaj) {
-  for (int x = threadIdx.x; x < 128 * WP; x += 128) {
-    const int r = x / WP, c = x % WP;
-    const __nv_bfloat16 val = (r < n && c < W) ? g[(r0 + r) * ld + (int64_t)h * W + c] : bz();
-    if (kmaj) *reinterpret_cast<__nv_bfloat16*>(kmaj + canon(r, c, WP)) = val;
-    if (mnmaj) *reinterpret_cast<__nv_bfloat16*>(mnmaj + canon_mn(r, c)) = val;
-  }
-}
-
 // Both backward kernels run 8 warps per 128-row tile: warps w and w + 4 share
 // TMEM lane quadrant w & 3 and split the 128 columns of S / dP (no row
 // reductions are needed in the backward: lse and delta are per row / column
 // inputs); the accumulators' columns are split between the two halves.
 constexpr int kBT = 2 * kM;  // threads of the backward kernels
 
-// stage rows [r0, r0+n) of a [S x (H*W)] bf16 tensor, head h, W valid of WP
-// columns, as a K-major [128 x WP] tile and (optionally) an MN-major
-// [WP x 128] tile (row index = k)
+// The CTA's own 128-row tile (loaded once), chunk-major, synchronously: one
+// 16-byte chunk per step on the vector path, element-wise otherwise.
 template <int WP>
-__device__ __forceinline__ void stage_rows8(const __nv_bfloat16* g, int64_t ld, int h, int W, int64_t r0, int n,
-                                            unsigned char* kmaj, unsigned char* mnmaj, int vec) {
-  if (vec) {  // one 16-byte chunk (8 elements) per step; both layouts take it as one 16-byte store
+__device__ __forceinline__ void stage_rows_tl(const __nv_bfloat16* g, int64_t ld, int h, int W, int64_t r0, int n,
+                                              unsigned char* dst, int vec) {
+  if (vec) {
     for (int x = threadIdx.x; x < 128 * (WP / 8); x += kBT) {
-      const int r = x / (WP / 8), c = (x % (WP / 8)) * 8;
+      const int r = x % 128, c = (x / 128) * 8;
       uint4 val = make_uint4(0, 0, 0, 0);
       if (r < n && c < W) val = __ldg(reinterpret_cast<const uint4*>(g + (r0 + r) * ld + (int64_t)h * W + c));
-      if (kmaj) *reinterpret_cast<uint4*>(kmaj + canon(r, c, WP)) = val;
-      if (mnmaj) *reinterpret_cast<uint4*>(mnmaj + canon_mn(r, c)) = val;
+      *reinterpret_cast<uint4*>(dst + tl(r, c)) = val;
     }
     return;
   }
   for (int x = threadIdx.x; x < 128 * WP; x += kBT) {
-    const int r = x / WP, c = x % WP;
+    const int r = x % 128, c = x / 128;
     const __nv_bfloat16 val = (r < n && c < W) ? g[(r0 + r) * ld + (int64_t)h * W + c] : bz();
-    if (kmaj) *reinterpret_cast<__nv_bfloat16*>(kmaj + canon(r, c, WP)) = val;
-    if (mnmaj) *reinterpret_cast<__nv_bfloat16*>(mnmaj + canon_mn(r, c)) = val;
-  }
-}
-
-// stage_rows8 through cp.async (no registers; completes at the caller's
-// cp_async_wait0): the backward kernels stage block j + 1 while block j
-// computes. Odd head widths fall back to the synchronous element-wise path.
-template <int WP>
-__device__ __forceinline__ void stage_rows8_async(const __nv_bfloat16* g, int64_t ld, int h, int W, int64_t r0, int n,
-                                                  unsigned char* kmaj, unsigned char* mnmaj, int vec) {
-  if (!vec) {
-    stage_rows8<WP>(g, ld, h, W, r0, n, kmaj, mnmaj, 0);
-    return;
-  }
-  for (int x = threadIdx.x; x < 128 * (WP / 8); x += kBT) {
-    const int r = x / (WP / 8), c = (x % (WP / 8)) * 8;
-    const bool ok = r < n && c < W;
-    const __nv_bfloat16* src = ok ? g + (r0 + r) * ld + (int64_t)h * W + c : g;
-    if (kmaj) cp_async16(kmaj + canon(r, c, WP), src, ok ? 16 : 0);
-    if (mnmaj) cp_async16(mnmaj + canon_mn(r, c), src, ok ? 16 : 0);
+    *reinterpret_cast<__nv_bfloat16*>(dst + tl(r, c)) = val;
   }
 }
 
@@ -631,19 +658,19 @@ __device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, float (&v)[NC]) {
 }
 
 template <int DKP, int DVP>
-__global__ void __launch_bounds__(kBT, 2) dense_tc_dq_kernel(TcBwdArgs a) {
+__global__ void __launch_bounds__(kBT, 2)
+    dense_tc_dq_kernel(TcBwdArgs a, const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV) {
   constexpr int kHN = kN / 2, kHK = DKP / 2;
   extern __shared__ __align__(1024) unsigned char smem[];
-  unsigned char* Qs = smem;                    // [128 x DKP] K-major (A of S)
-  unsigned char* Ds = Qs + kM * DKP * 2;       // [128 x DVP] K-major (A of dP)
-  // key-block operands, double-buffered: [K | V | Km] per buffer
-  constexpr int kKB = kN * DKP * 2 + kN * DVP * 2 + DKP * kN * 2;
-  unsigned char* KB = Ds + kM * DVP * 2;       // 2 x {K [128 keys x DKP] K-major (B of S),
-                                               //      V [128 keys x DVP] K-major (B of dP),
-                                               //      Km [DKP x 128 keys] MN-major (B of dQ)}
+  unsigned char* Qs = smem;                    // [128 x DKP] chunk-major (A of S)
+  unsigned char* Ds = Qs + kM * DKP * 2;       // [128 x DVP] chunk-major (A of dP)
+  // key-block operands, double-buffered, chunk-major: [K | V] per buffer
+  constexpr int kKB = kN * DKP * 2 + kN * DVP * 2;
+  unsigned char* KB = Ds + kM * DVP * 2;       // 2 x {K [128 keys x DKP] (K-major B of S, MN-major B of dQ),
+                                               //      V [128 keys x DVP] (K-major B of dP)}
   unsigned char* dS = KB + 2 * kKB;            // [128 x 128] K-major (A of dQ)
-  uint64_t* bar = reinterpret_cast<uint64_t*>(dS + kM * kN * 2);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(dS + kM * kN * 2);  // [0] MMA, [1 + b] TMA of buffer b
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 3);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, quad = warp & 3, half = warp >> 2;
   const int rl = quad * 32 + lane, cb = half * kHN, h = blockIdx.y;
   const int64_t r0 = (int64_t)blockIdx.x * kM, row = r0 + rl;
@@ -654,12 +681,22 @@ __global__ void __launch_bounds__(kBT, 2) dense_tc_dq_kernel(TcBwdArgs a) {
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)));
+    for (int b = 0; b < 3; ++b) mbar_init(bar + b);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (a.vec) {
+      tma_prefetch(&tmK);
+      tma_prefetch(&tmV);
+    }
   }
   const int nq = (int)(a.s_real - r0 < kM ? (a.s_real - r0 > 0 ? a.s_real - r0 : 0) : kM);
-  stage_rows8<DKP>(a.q, a.ldq, h, a.dk, r0, nq, Qs, nullptr, a.vec);
-  stage_rows8<DVP>(a.dout, a.ldv, h, a.dv, r0, nq, Ds, nullptr, a.vec);
+  stage_rows_tl<DKP>(a.q, a.ldq, h, a.dk, r0, nq, Qs, a.vec);
+  stage_rows_tl<DVP>(a.dout, a.ldv, h, a.dv, r0, nq, Ds, a.vec);
+  if (a.vec) {
+    for (int b = 0; b < 2; ++b) {
+      zero_pad_chunks<DKP>(KB + b * kKB, a.dk, kBT);
+      zero_pad_chunks<DVP>(KB + b * kKB + kN * DKP * 2, a.dv, kBT);
+    }
+  }
   float lse = 0.f, delta = 0.f;
   if (real) {
     lse = a.lse[row * a.H + h];
@@ -674,22 +711,31 @@ __global__ void __launch_bounds__(kBT, 2) dense_tc_dq_kernel(TcBwdArgs a) {
   const uint32_t tmem = *tmem_slot, t_row = tmem + ((uint32_t)(quad * 32) << 16);
   const uint32_t sQ = (uint32_t)__cvta_generic_to_shared(Qs), sD = (uint32_t)__cvta_generic_to_shared(Ds);
   const uint32_t sKB = (uint32_t)__cvta_generic_to_shared(KB), sS = (uint32_t)__cvta_generic_to_shared(dS);
-  auto stage_keys = [&](int64_t c, int b) {
+  auto stage_keys = [&](int64_t c, int b) {  // one TMA barrier per buffer: K and V chunks
     const int nn = (int)(a.s_real - c < kN ? a.s_real - c : kN);
     unsigned char* base = KB + b * kKB;
-    stage_rows8_async<DKP>(a.k, a.ldq, h, a.dk, c, nn, base, base + kN * DKP * 2 + kN * DVP * 2, a.vec);
-    stage_rows8_async<DVP>(a.v, a.ldv, h, a.dv, c, nn, base + kN * DKP * 2, nullptr, a.vec);
-    cp_async_commit();
+    if (a.vec) {
+      if (tid == 0) {
+        mbar_expect_tx(bar + 1 + b, (uint32_t)(a.dk / 8 + a.dv / 8) * 2048u);
+        for (int x = 0; x < a.dk / 8; ++x) tma_chunk(base + x * 2048, &tmK, h * a.dk + x * 8, (int)c, bar + 1 + b);
+        for (int x = 0; x < a.dv / 8; ++x)
+          tma_chunk(base + kN * DKP * 2 + x * 2048, &tmV, h * a.dv + x * 8, (int)c, bar + 1 + b);
+      }
+      return;
+    }
+    stage_tl<DKP>(&tmK, a.k, a.ldq, h, a.dk, c, nn, base, nullptr, 0, kBT);
+    stage_tl<DVP>(&tmV, a.v, a.ldv, h, a.dv, c, nn, base + kN * DKP * 2, nullptr, 0, kBT);
   };
   uint32_t phase = 0;
   const bool rows_full = r0 + kM <= a.s_real;  // CTA-uniform
   const uint64_t sc2 = pk2(a.scale_l, a.scale_l), nl2 = pk2(-lse, -lse), nd2 = pk2(-delta, -delta);
   if (a.s_real > 0) stage_keys(0, 0);
   int buf = 0;
-  for (int64_t c0 = 0; c0 < a.s_real; c0 += kN, buf ^= 1) {
+  uint32_t blk = 0;
+  for (int64_t c0 = 0; c0 < a.s_real; c0 += kN, buf ^= 1, ++blk) {
     const int n = (int)(a.s_real - c0 < kN ? a.s_real - c0 : kN);
-    const uint32_t sK = sKB + (uint32_t)(buf * kKB), sV = sK + kN * DKP * 2, sKm = sV + kN * DVP * 2;
-    cp_async_wait0();  // this block's keys (issued one block ahead)
+    const uint32_t sK = sKB + (uint32_t)(buf * kKB), sV = sK + kN * DKP * 2;
+    if (a.vec) mbar_wait(bar + 1 + buf, (blk >> 1) & 1);  // this block's keys (issued one block ahead)
     fence_async_smem();
     tc_before_sync();
     __syncthreads();
@@ -697,9 +743,7 @@ __global__ void __launch_bounds__(kBT, 2) dense_tc_dq_kernel(TcBwdArgs a) {
     if (c0 + kN < a.s_real) stage_keys(c0 + kN, buf ^ 1);  // the other buffer's MMAs completed last block
     if (tid == 0) {  // S = Q K^T
 #pragma unroll
-      for (int kc = 0; kc < DKP / 16; ++kc)
-        mma_bf16(tmem, smem_desc(sQ + kc * 256, 128, DKP * 16), smem_desc(sK + kc * 256, 128, DKP * 16),
-                 instr_desc(kM, kN), kc > 0);
+      for (int kc = 0; kc < DKP / 16; ++kc) mma_bf16(tmem, kdesc(sQ, kc), kdesc(sK, kc), instr_desc(kM, kN), kc > 0);
       mma_commit(bar);
     }
     mbar_wait(bar, phase);
@@ -734,9 +778,7 @@ __global__ void __launch_bounds__(kBT, 2) dense_tc_dq_kernel(TcBwdArgs a) {
     tc_after_sync();
     if (tid == 0) {  // dP = dO V^T (same TMEM columns; S is in registers)
 #pragma unroll
-      for (int kc = 0; kc < DVP / 16; ++kc)
-        mma_bf16(tmem, smem_desc(sD + kc * 256, 128, DVP * 16), smem_desc(sV + kc * 256, 128, DVP * 16),
-                 instr_desc(kM, kN), kc > 0);
+      for (int kc = 0; kc < DVP / 16; ++kc) mma_bf16(tmem, kdesc(sD, kc), kdesc(sV, kc), instr_desc(kM, kN), kc > 0);
       mma_commit(bar);
     }
     mbar_wait(bar, phase);
@@ -766,8 +808,8 @@ __global__ void __launch_bounds__(kBT, 2) dense_tc_dq_kernel(TcBwdArgs a) {
     if (tid == 0) {  // dQ += dS K  (A = dS K-major, B = K MN-major, N = DKP)
 #pragma unroll
       for (int kc = 0; kc < kN / 16; ++kc)
-        mma_bf16(tmem + 128, smem_desc(sS + kc * 256, 128, kN * 16), smem_desc(sKm + kc * 256, 128, 2048),
-                 instr_desc_bmn(kM, DKP), (c0 > 0 || kc > 0) ? 1u : 0u);
+        mma_bf16(tmem + 128, smem_desc(sS + kc * 256, 128, kN * 16), mndesc(sK, kc), instr_desc_bmn(kM, DKP),
+                 (c0 > 0 || kc > 0) ? 1u : 0u);
       mma_commit(bar);
     }
     mbar_wait(bar, phase);
@@ -792,22 +834,21 @@ __global__ void __launch_bounds__(kBT, 2) dense_tc_dq_kernel(TcBwdArgs a) {
 }
 
 template <int DKP, int DVP>
-__global__ void __launch_bounds__(kBT, 2) dense_tc_dkdv_kernel(TcBwdArgs a) {
+__global__ void __launch_bounds__(kBT, 2)
+    dense_tc_dkdv_kernel(TcBwdArgs a, const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmD) {
   constexpr int kHN = kN / 2, kHK = DKP / 2, kHV = DVP / 2;
   extern __shared__ __align__(1024) unsigned char smem[];
-  unsigned char* Ks = smem;                    // [128 keys x DKP] K-major (A of S^T)
-  unsigned char* Vs = Ks + kM * DKP * 2;       // [128 keys x DVP] K-major (A of dP^T)
-  // query-block operands, double-buffered: [Qk | Dk | Qm | Dm | lse | delta] per buffer
-  constexpr int kQB = (kN * DKP + kN * DVP + DKP * kN + DVP * kN) * 2 + 2 * kN * 4;
-  unsigned char* QB = Vs + kM * DVP * 2;       // 2 x {Qk [128 q x DKP] K-major (B of S^T),
-                                               //      Dk [128 q x DVP] K-major (B of dP^T),
-                                               //      Qm [DKP x 128 q] MN-major (B of dK),
-                                               //      Dm [DVP x 128 q] MN-major (B of dV),
+  unsigned char* Ks = smem;                    // [128 keys x DKP] chunk-major (A of S^T)
+  unsigned char* Vs = Ks + kM * DKP * 2;       // [128 keys x DVP] chunk-major (A of dP^T)
+  // query-block operands, double-buffered: [Q | dO | lse | delta] per buffer
+  constexpr int kQB = (kN * DKP + kN * DVP) * 2 + 2 * kN * 4;
+  unsigned char* QB = Vs + kM * DVP * 2;       // 2 x {Q [128 q x DKP] chunk-major (K-major B of S^T, MN-major B of dK),
+                                               //      dO [128 q x DVP] chunk-major (K-major B of dP^T, MN-major B of dV),
                                                //      lse [128], delta [128] of the query block}
   unsigned char* Pt = QB + 2 * kQB;            // [128 keys x 128 q] K-major (A of dV)
   unsigned char* St = Pt + kM * kN * 2;        // [128 keys x 128 q] K-major (A of dK)
-  uint64_t* bar = reinterpret_cast<uint64_t*>(St + kM * kN * 2);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(St + kM * kN * 2);  // [0] MMA, [1 + b] TMA of buffer b
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 3);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, quad = warp & 3, half = warp >> 2;
   const int rl = quad * 32 + lane, cb = half * kHN, h = blockIdx.y;
   const int64_t k0 = (int64_t)blockIdx.x * kM, key = k0 + rl;
@@ -818,12 +859,22 @@ __global__ void __launch_bounds__(kBT, 2) dense_tc_dkdv_kernel(TcBwdArgs a) {
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)));
+    for (int b = 0; b < 3; ++b) mbar_init(bar + b);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (a.vec) {
+      tma_prefetch(&tmQ);
+      tma_prefetch(&tmD);
+    }
   }
   const int nk = (int)(a.s_real - k0 < kM ? (a.s_real - k0 > 0 ? a.s_real - k0 : 0) : kM);
-  stage_rows8<DKP>(a.k, a.ldq, h, a.dk, k0, nk, Ks, nullptr, a.vec);
-  stage_rows8<DVP>(a.v, a.ldv, h, a.dv, k0, nk, Vs, nullptr, a.vec);
+  stage_rows_tl<DKP>(a.k, a.ldq, h, a.dk, k0, nk, Ks, a.vec);
+  stage_rows_tl<DVP>(a.v, a.ldv, h, a.dv, k0, nk, Vs, a.vec);
+  if (a.vec) {
+    for (int b = 0; b < 2; ++b) {
+      zero_pad_chunks<DKP>(QB + b * kQB, a.dk, kBT);
+      zero_pad_chunks<DVP>(QB + b * kQB + kN * DKP * 2, a.dv, kBT);
+    }
+  }
   tc_before_sync();
   __syncthreads();
   tc_after_sync();
@@ -832,12 +883,21 @@ __global__ void __launch_bounds__(kBT, 2) dense_tc_dkdv_kernel(TcBwdArgs a) {
   const uint32_t sQB = (uint32_t)__cvta_generic_to_shared(QB);
   const uint32_t sPt = (uint32_t)__cvta_generic_to_shared(Pt), sSt = (uint32_t)__cvta_generic_to_shared(St);
   constexpr uint32_t kColV = 128, kColK = 192;  // dV, dK accumulators
-  constexpr int oDk = kN * DKP * 2, oQm = oDk + kN * DVP * 2, oDm = oQm + DKP * kN * 2, oLs = oDm + DVP * kN * 2;
+  constexpr int oDk = kN * DKP * 2, oLs = oDk + kN * DVP * 2;
   auto stage_queries = [&](int64_t q, int b) {
     const int nn = (int)(a.s_real - q < kN ? a.s_real - q : kN);
     unsigned char* base = QB + b * kQB;
-    stage_rows8_async<DKP>(a.q, a.ldq, h, a.dk, q, nn, base, base + oQm, a.vec);
-    stage_rows8_async<DVP>(a.dout, a.ldv, h, a.dv, q, nn, base + oDk, base + oDm, a.vec);
+    if (a.vec) {
+      if (tid == 0) {
+        mbar_expect_tx(bar + 1 + b, (uint32_t)(a.dk / 8 + a.dv / 8) * 2048u);
+        for (int x = 0; x < a.dk / 8; ++x) tma_chunk(base + x * 2048, &tmQ, h * a.dk + x * 8, (int)q, bar + 1 + b);
+        for (int x = 0; x < a.dv / 8; ++x)
+          tma_chunk(base + oDk + x * 2048, &tmD, h * a.dv + x * 8, (int)q, bar + 1 + b);
+      }
+    } else {
+      stage_tl<DKP>(&tmQ, a.q, a.ldq, h, a.dk, q, nn, base, nullptr, 0, kBT);
+      stage_tl<DVP>(&tmD, a.dout, a.ldv, h, a.dv, q, nn, base + oDk, nullptr, 0, kBT);
+    }
     if (tid < kN) {  // lse, delta (the dq kernel's dO . O) of the block's queries; zeros past the end
       const bool ok = tid < nn;
       const int64_t qr = ok ? q + tid : 0;
@@ -851,12 +911,14 @@ __global__ void __launch_bounds__(kBT, 2) dense_tc_dkdv_kernel(TcBwdArgs a) {
   const bool keys_full = k0 + kM <= a.s_real;  // CTA-uniform
   if (a.s_real > 0) stage_queries(0, 0);
   int buf = 0;
-  for (int64_t q0 = 0; q0 < a.s_real; q0 += kN, buf ^= 1) {
+  uint32_t blk = 0;
+  for (int64_t q0 = 0; q0 < a.s_real; q0 += kN, buf ^= 1, ++blk) {
     const int n = (int)(a.s_real - q0 < kN ? a.s_real - q0 : kN);
-    const uint32_t sQk = sQB + (uint32_t)(buf * kQB), sDk = sQk + oDk, sQm = sQk + oQm, sDm = sQk + oDm;
+    const uint32_t sQk = sQB + (uint32_t)(buf * kQB), sDk = sQk + oDk;
     const float* ls = reinterpret_cast<const float*>(QB + buf * kQB + oLs);
     const float* dl = ls + kN;
-    cp_async_wait0();  // this block's queries (issued one block ahead)
+    cp_async_wait0();                                     // this block's lse / delta
+    if (a.vec) mbar_wait(bar + 1 + buf, (blk >> 1) & 1);  // and its Q / dO tiles (issued one block ahead)
     fence_async_smem();
     tc_before_sync();
     __syncthreads();
@@ -865,8 +927,7 @@ __global__ void __launch_bounds__(kBT, 2) dense_tc_dkdv_kernel(TcBwdArgs a) {
     if (tid == 0) {  // S^T = K Q^T
 #pragma unroll
       for (int kc = 0; kc < DKP / 16; ++kc)
-        mma_bf16(tmem, smem_desc(sK + kc * 256, 128, DKP * 16), smem_desc(sQk + kc * 256, 128, DKP * 16),
-                 instr_desc(kM, kN), kc > 0);
+        mma_bf16(tmem, kdesc(sK, kc), kdesc(sQk, kc), instr_desc(kM, kN), kc > 0);
       mma_commit(bar);
     }
     mbar_wait(bar, phase);
@@ -916,8 +977,7 @@ __global__ void __launch_bounds__(kBT, 2) dense_tc_dkdv_kernel(TcBwdArgs a) {
     if (tid == 0) {  // dP^T = V dO^T
 #pragma unroll
       for (int kc = 0; kc < DVP / 16; ++kc)
-        mma_bf16(tmem, smem_desc(sV + kc * 256, 128, DVP * 16), smem_desc(sDk + kc * 256, 128, DVP * 16),
-                 instr_desc(kM, kN), kc > 0);
+        mma_bf16(tmem, kdesc(sV, kc), kdesc(sDk, kc), instr_desc(kM, kN), kc > 0);
       mma_commit(bar);
     }
     mbar_wait(bar, phase);
@@ -948,11 +1008,11 @@ __global__ void __launch_bounds__(kBT, 2) dense_tc_dkdv_kernel(TcBwdArgs a) {
     if (tid == 0) {  // dV += P^T dO, dK += dS^T Q
 #pragma unroll
       for (int kc = 0; kc < kN / 16; ++kc)
-        mma_bf16(tmem + kColV, smem_desc(sPt + kc * 256, 128, kN * 16), smem_desc(sDm + kc * 256, 128, 2048),
+        mma_bf16(tmem + kColV, smem_desc(sPt + kc * 256, 128, kN * 16), mndesc(sDk, kc),
                  instr_desc_bmn(kM, DVP), (q0 > 0 || kc > 0) ? 1u : 0u);
 #pragma unroll
       for (int kc = 0; kc < kN / 16; ++kc)
-        mma_bf16(tmem + kColK, smem_desc(sSt + kc * 256, 128, kN * 16), smem_desc(sQm + kc * 256, 128, 2048),
+        mma_bf16(tmem + kColK, smem_desc(sSt + kc * 256, 128, kN * 16), mndesc(sQk, kc),
                  instr_desc_bmn(kM, DKP), (q0 > 0 || kc > 0) ? 1u : 0u);
       mma_commit(bar);
     }
@@ -994,19 +1054,23 @@ __global__ void __launch_bounds__(kBT, 2) dense_tc_dkdv_kernel(TcBwdArgs a) {
 
 template <int DKP, int DVP>
 cudaError_t launch_bwd(const TcBwdArgs& a, cudaStream_t st) {
-  const size_t s1 = (size_t)kM * (DKP + DVP) * 2 + 2 * ((size_t)kN * (DKP + DVP) * 2 + (size_t)DKP * kN * 2) +
-                    (size_t)kM * kN * 2 + 16;
-  const size_t s2 = (size_t)kM * (DKP + DVP) * 2 +
-                    2 * ((size_t)kN * (DKP + DVP) * 2 + (size_t)(DKP + DVP) * kN * 2 + 2 * kN * 4) +
-                    2 * (size_t)kM * kN * 2 + 16;
+  const size_t s1 = (size_t)kM * (DKP + DVP) * 2 + 2 * (size_t)kN * (DKP + DVP) * 2 + (size_t)kM * kN * 2 + 32;
+  const size_t s2 = (size_t)kM * (DKP + DVP) * 2 + 2 * ((size_t)kN * (DKP + DVP) * 2 + 2 * kN * 4) +
+                    2 * (size_t)kM * kN * 2 + 32;
+  CUtensorMap tq{}, tk{}, tv{}, td{};
+  if (a.vec && !(encode_rows_map(&tq, a.q, (int64_t)a.H * a.dk, a.s_real, a.ldq) &&
+                 encode_rows_map(&tk, a.k, (int64_t)a.H * a.dk, a.s_real, a.ldq) &&
+                 encode_rows_map(&tv, a.v, (int64_t)a.H * a.dv, a.s_real, a.ldv) &&
+                 encode_rows_map(&td, a.dout, (int64_t)a.H * a.dv, a.s_real, a.ldv)))
+    return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(dense_tc_dq_kernel<DKP, DVP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)s1);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(dense_tc_dkdv_kernel<DKP, DVP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2);
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)((a.S + kM - 1) / kM), (unsigned)a.H);
-  dense_tc_dq_kernel<DKP, DVP><<<grid, kBT, s1, st>>>(a);
-  dense_tc_dkdv_kernel<DKP, DVP><<<grid, kBT, s2, st>>>(a);
+  dense_tc_dq_kernel<DKP, DVP><<<grid, kBT, s1, st>>>(a, tk, tv);
+  dense_tc_dkdv_kernel<DKP, DVP><<<grid, kBT, s2, st>>>(a, tq, td);
   return cudaGetLastError();
 }
 
