@@ -28,6 +28,18 @@ __device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
   return d;
 }
 
+// acc[0..N) *= c on FMUL2 (the online-softmax rescale)
+template <int N>
+__device__ __forceinline__ void scale_pairs(float (&acc)[N], float c) {
+  const uint64_t cc = pk(c, c);
+#pragma unroll
+  for (int i = 0; i < N / 2; ++i) {
+    uint64_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk(acc[2 * i], acc[2 * i + 1])), "l"(cc));
+    upk(r, acc[2 * i], acc[2 * i + 1]);
+  }
+}
+
 template <typename T> struct Piece;
 
 // f32: 4 elements per 16-byte piece
@@ -91,7 +103,32 @@ template <> struct Piece<__nv_bfloat16> {
       upk(r, acc[2 * i], acc[2 * i + 1]);
     }
   }
-  __device__ __forceinline__ static void axpy_w(float w, const uint4& x, float (&acc)[8]) { axpy(w, x, acc); }
+#ifndef GTE_BF16_AXPY_FHFMA
+#define GTE_BF16_AXPY_FHFMA 1
+#endif
+  // acc[0..7] += w * x for the per-edge weights (p, dS) of the gather loops.
+  // With GTE_BF16_AXPY_FHFMA the weight is rounded to bf16 — the precision
+  // the P / dS operands have in FlashAttention-style bf16 kernels (and in
+  // dense_tc.cu) — and the update runs on FHFMA.BF16 (bf16 operands, fp32
+  // accumulate, no unpacking): 1 cvt + 8 FHFMA per edge instead of 8 unpack
+  // + 4 FFMA2.
+  __device__ __forceinline__ static void axpy_w(float w, const uint4& x, float (&acc)[8]) {
+#if GTE_BF16_AXPY_FHFMA
+    asm("{.reg .b16 wb, l0, h0, l1, h1, l2, h2, l3, h3;\n\t"
+        "cvt.rn.bf16.f32 wb, %8;\n\t"
+        "mov.b32 {l0, h0}, %9;\n\tmov.b32 {l1, h1}, %10;\n\t"
+        "mov.b32 {l2, h2}, %11;\n\tmov.b32 {l3, h3}, %12;\n\t"
+        "fma.rn.f32.bf16 %0, wb, l0, %0;\n\tfma.rn.f32.bf16 %1, wb, h0, %1;\n\t"
+        "fma.rn.f32.bf16 %2, wb, l1, %2;\n\tfma.rn.f32.bf16 %3, wb, h1, %3;\n\t"
+        "fma.rn.f32.bf16 %4, wb, l2, %4;\n\tfma.rn.f32.bf16 %5, wb, h2, %5;\n\t"
+        "fma.rn.f32.bf16 %6, wb, l3, %6;\n\tfma.rn.f32.bf16 %7, wb, h3, %7;}"
+        : "+f"(acc[0]), "+f"(acc[1]), "+f"(acc[2]), "+f"(acc[3]), "+f"(acc[4]), "+f"(acc[5]), "+f"(acc[6]),
+          "+f"(acc[7])
+        : "f"(w), "r"(x.x), "r"(x.y), "r"(x.z), "r"(x.w));
+#else
+    axpy(w, x, acc);
+#endif
+  }
   __device__ __forceinline__ static float finite_probe(const uint4& x, float chk) {
     // a bf16 pair is non-finite iff one of its exponent fields is all ones
     const uint32_t u[4] = {x.x, x.y, x.z, x.w};
