@@ -538,12 +538,43 @@ class DeviceDenseAttention:
         self.ctx = ctx or Context.get()
         self.code = _lib.DTYPES[dtype]
 
+    def _check(self, qk, vo, acc=()):
+        """The C ABI takes one row stride for the Q-shaped tensors (q, k and
+        the dq, dk it writes) and one for the V-shaped ones (v, out, dout,
+        dv): they must agree, rows must be unit-stride, dtypes must match this
+        instance and everything must sit on the context's CUDA device."""
+        import torch
+
+        want = getattr(torch, _TORCH_DT[self.dtype])
+        acc_t = torch.float64 if self.dtype == "f64" else torch.float32
+        for group, width, name in ((qk, self.H * self.dk, "q/k"), (vo, self.H * self.dv, "v/out")):
+            ld = None
+            for t in group:
+                if t.dtype != want:
+                    raise ConfigError(f"dense_attention: {name} tensor dtype {t.dtype} != {want}")
+                if t.dim() != 2 or t.shape[0] != self.S or t.shape[1] != width or t.stride(1) != 1:
+                    raise ConfigError(f"dense_attention: {name} tensors must be [S, {width}] with unit column stride")
+                if ld is None:
+                    ld = t.stride(0)
+                elif t.stride(0) != ld:
+                    raise ConfigError(f"dense_attention: {name} tensors must share one row stride")
+                if t.device.type != "cuda" or t.device.index != self.ctx.device:
+                    raise ConfigError("dense_attention: tensors are not on the context's CUDA device")
+        for t in acc:
+            if t is None:
+                continue
+            if t.dtype not in (acc_t, torch.uint8) or not t.is_contiguous():
+                raise ConfigError(f"dense_attention: lse/bias/weight_mult/buckets must be contiguous {acc_t}")
+            if t.device.type != "cuda" or t.device.index != self.ctx.device:
+                raise ConfigError("dense_attention: tensors are not on the context's CUDA device")
+
     def forward(self, q, k, v, bias=None, weight_mult=None):
         import torch
 
+        self._check((q, k), (v,), (bias, weight_mult))
         L = _bind_dense()
         acc = torch.float64 if self.dtype == "f64" else torch.float32
-        out = torch.empty((self.S, self.H * self.dv), dtype=v.dtype, device=v.device)
+        out = torch.empty_strided(v.shape, v.stride(), dtype=v.dtype, device=v.device)  # written with v's row stride
         lse = torch.empty((self.S, self.H), dtype=acc, device=v.device)
         self.ctx.set_stream(torch.cuda.current_stream().cuda_stream)
         check(L.gte_dense_attn_fwd(self.ctx.h, self.code, self.S, self.s_real, self.H, self.dk, self.dv, q.data_ptr(),
@@ -558,7 +589,8 @@ class DeviceDenseAttention:
 
         L = _bind_dense()
         acc = torch.float64 if self.dtype == "f64" else torch.float32
-        dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+        self._check((q, k), (v, out, dout), (lse, bias, weight_mult))
+        dq, dk, dv = (torch.empty_strided(x.shape, x.stride(), dtype=x.dtype, device=x.device) for x in (q, k, v))
         db = torch.empty((self.S, self.S), dtype=acc, device=q.device) if want_dbias else None
         self.ctx.set_stream(torch.cuda.current_stream().cuda_stream)
         check(L.gte_dense_attn_bwd(self.ctx.h, self.code, self.S, self.s_real, self.H, self.dk, self.dv, q.data_ptr(),
@@ -574,9 +606,10 @@ class DeviceDenseAttention:
     def forward_buckets(self, q, k, v, buckets, table, weight_mult=None):
         import torch
 
+        self._check((q, k), (v,), (buckets, table, weight_mult))
         L = _bind_dense()
         acc = torch.float64 if self.dtype == "f64" else torch.float32
-        out = torch.empty((self.S, self.H * self.dv), dtype=v.dtype, device=v.device)
+        out = torch.empty_strided(v.shape, v.stride(), dtype=v.dtype, device=v.device)
         lse = torch.empty((self.S, self.H), dtype=acc, device=v.device)
         self.ctx.set_stream(torch.cuda.current_stream().cuda_stream)
         check(L.gte_dense_attn_fwd_buckets(self.ctx.h, self.code, self.S, self.s_real, self.H, self.dk, self.dv,
@@ -589,8 +622,9 @@ class DeviceDenseAttention:
     def backward_buckets(self, q, k, v, out, lse, dout, buckets, table, weight_mult=None):
         import torch
 
+        self._check((q, k), (v, out, dout), (lse, buckets, table, weight_mult))
         L = _bind_dense()
-        dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+        dq, dk, dv = (torch.empty_strided(x.shape, x.stride(), dtype=x.dtype, device=x.device) for x in (q, k, v))
         dtable = torch.empty_like(table)
         self.ctx.set_stream(torch.cuda.current_stream().cuda_stream)
         check(L.gte_dense_attn_bwd_buckets(self.ctx.h, self.code, self.S, self.s_real, self.H, self.dk, self.dv,

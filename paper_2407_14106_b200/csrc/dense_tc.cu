@@ -283,6 +283,7 @@ __global__ void __launch_bounds__(2 * kM, (DKP <= 16 && DVP <= 16) ? 4 : 3)
   float* red = reinterpret_cast<float*>(Ps + kM * kN * 2);  // [2][128] partial maxima / sums
   uint64_t* bar = reinterpret_cast<uint64_t*>(red + 2 * kM);  // [0] MMA commits, [1 + b] TMA of buffer b
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 3);
+  int* s_flag = reinterpret_cast<int*>(tmem_slot + 1);  // last block whose scores outran the running max
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int quad = warp & 3, half = warp >> 2;
@@ -303,6 +304,7 @@ __global__ void __launch_bounds__(2 * kM, (DKP <= 16 && DVP <= 16) ? 4 : 3)
       tma_prefetch(&tmK);
       tma_prefetch(&tmV);
     }
+    *s_flag = -1;
   }
   for (int x = tid; x < kM * DKP; x += kT) {
     const int r = x % kM, kk = x / kM;
@@ -361,6 +363,51 @@ __global__ void __launch_bounds__(2 * kM, (DKP <= 16 && DVP <= 16) ? 4 : 3)
     // BW is off): no per-element masks, packed FFMA2 / FADD2 (the softmax
     // passes are issue-bound; the masks were ~40 % of their instructions).
     if (!BW && n == kN) {
+      // After the first block: ONE pass against the running max m (FA4's
+      // conditional rescale) — p = 2^(s - m) <= 2^8 unless a score outruns m
+      // by more than 8 (log2 units), in which case the whole CTA redoes the
+      // block below with the exact max. Saves the max pass over TMEM and its
+      // row reduction through shared memory on almost every block.
+      bool fast = false;
+      float corr = 1.f;
+      if (blk > 0) {
+        const uint64_t sc2 = pk2(a.scale_l, a.scale_l), nm2 = pk2(-m, -m);
+        uint64_t l2 = pk2(0.f, 0.f);
+        float mx = -INFINITY;
+#pragma unroll
+        for (int q4 = 0; q4 < kHalfN / 16; ++q4) {
+          float v16[16];
+          tmem_ld16(t_row + cbase + q4 * 16, v16);
+#pragma unroll
+          for (int c8 = 0; c8 < 2; ++c8) {
+            uint32_t w[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int j = c8 * 8 + 2 * i;
+              mx = fmaxf(mx, fmaxf(v16[j], v16[j + 1]));
+              float x0, x1;
+              upk2(fma2(pk2(v16[j], v16[j + 1]), sc2, nm2), x0, x1);
+              const float p0 = ex2_approx(x0), p1 = ex2_approx(x1);
+              l2 = add2(l2, pk2(p0, p1));
+              w[i] = bf16x2(p0, p1);
+            }
+            *reinterpret_cast<uint4*>(Ps + canon(rl, cbase + q4 * 16 + c8 * 8, kN)) =
+                make_uint4(w[0], w[1], w[2], w[3]);
+          }
+        }
+        if (mx * a.scale_l > m + 8.f) *s_flag = (int)blk;
+        fence_async_smem();
+        tc_before_sync();
+        __syncthreads();
+        tc_after_sync();
+        fast = *s_flag != (int)blk;  // CTA-uniform
+        if (fast) {
+          float la, lb;
+          upk2(l2, la, lb);
+          l += la + lb;
+        }
+      }
+      if (!fast) {
       float mx = -INFINITY;
 #pragma unroll
       for (int q4 = 0; q4 < kHalfN / 16; ++q4) {
@@ -372,7 +419,7 @@ __global__ void __launch_bounds__(2 * kM, (DKP <= 16 && DVP <= 16) ? 4 : 3)
       red[half * kM + rl] = mx * a.scale_l;
       __syncthreads();
       const float mn = fmaxf(m, fmaxf(red[rl], red[kM + rl]));
-      const float corr = ex2_approx(m - mn);
+      corr = ex2_approx(m - mn);
       const uint64_t sc2 = pk2(a.scale_l, a.scale_l), nm2 = pk2(-mn, -mn);
       uint64_t l2 = pk2(0.f, 0.f);
 #pragma unroll
@@ -403,6 +450,7 @@ __global__ void __launch_bounds__(2 * kM, (DKP <= 16 && DVP <= 16) ? 4 : 3)
       tc_before_sync();
       __syncthreads();
       tc_after_sync();
+      }
       if (tid == 0) {
 #pragma unroll
         for (int kc = 0; kc < kN / 16; ++kc)

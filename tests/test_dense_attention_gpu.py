@@ -186,3 +186,65 @@ def test_tcgen05_many_blocks_vs_torch_fp32(cuda, S, s_real, H, dh):
     close(f(dq)[:s_real], rg(qf)[:s_real], "bf16", "dq")
     close(f(dk)[:s_real], rg(kf)[:s_real], "bf16", "dk")
     close(f(dv), rg(vf), "bf16", "dv")
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_strided_fused_qkv_matches_contiguous(cuda, dtype):
+    """q, k, v as column slices of one fused [S, 3 d] tensor (row stride 3 d):
+    the C ABI takes one row stride per tensor family, so the outputs must be
+    allocated with the inputs' strides — results equal the contiguous call's
+    bit for bit. Mismatched dtypes / strides raise ConfigError."""
+    import torch
+
+    S, H, dh = 300, 2, 8
+    d = H * dh
+    t = {"bf16": torch.bfloat16, "f32": torch.float32}[dtype]
+    g = torch.Generator(device="cuda").manual_seed(7)
+    qkv = torch.randn((S, 3 * d), generator=g, device="cuda").to(t)
+    up = torch.randn((S, d), generator=g, device="cuda").to(t)
+    q, k, v = qkv[:, :d], qkv[:, d:2 * d], qkv[:, 2 * d:]
+    att = A.DeviceDenseAttention(S, H, dh, dh, dtype)
+    o1, l1 = att.forward(q, k, v)
+    qc, kc, vc = q.contiguous(), k.contiguous(), v.contiguous()
+    o2, l2 = att.forward(qc, kc, vc)
+    torch.cuda.synchronize()
+    assert o1.stride() == v.stride()
+    assert torch.equal(o1, o2) and torch.equal(l1, l2)
+    # backward: dO and O with V's row stride, as the ABI requires
+    do = torch.empty_strided(v.shape, v.stride(), dtype=t, device="cuda").copy_(up)
+    dq1, dk1, dv1, _ = att.backward(q, k, v, o1, l1, do)
+    dq2, dk2, dv2, _ = att.backward(qc, kc, vc, o2, l2, up)
+    torch.cuda.synchronize()
+    assert dq1.stride() == q.stride() and dv1.stride() == v.stride()
+    for a_, b_ in ((dq1, dq2), (dk1, dk2), (dv1, dv2)):
+        assert torch.equal(a_, b_)
+    with pytest.raises(ConfigError):
+        att.forward(q.float() if dtype == "bf16" else q.double(), k, v)
+    with pytest.raises(ConfigError):
+        att.backward(q, k, v, o1, l1, up)  # dO contiguous, O strided: two row strides
+
+
+@pytest.mark.parametrize("boost_at", [384, 1000])
+def test_tcgen05_forward_running_max_overrun(cuda, boost_at):
+    """The forward's one-pass blocks score against the running max and redo a
+    block exactly when a score outruns it by more than 8 (log2 units). Keys
+    from `boost_at` on are scaled x 24, so later blocks overrun the max of the
+    earlier ones by far more than 8: the redo path must give the same softmax
+    as a torch fp32 restatement (bf16 tolerance 2e-2 / 1e-2)."""
+    import torch
+
+    S, H, dh = 1280, 2, 8
+    g = torch.Generator(device="cuda").manual_seed(boost_at)
+    q, k, v = (torch.randn((S, H * dh), generator=g, device="cuda") for _ in range(3))
+    k[boost_at:] *= 24.0
+    q, k, v = (t.to(torch.bfloat16) for t in (q, k, v))
+    att = A.DeviceDenseAttention(S, H, dh, dh, "bf16")
+    out, lse = att.forward(q, k, v)
+    torch.cuda.synchronize()
+    qf, kf, vf = (t.float().view(S, H, dh).transpose(0, 1) for t in (q, k, v))
+    logits = qf @ kf.transpose(1, 2) / dh ** 0.5
+    ref = (torch.softmax(logits, dim=-1) @ vf).transpose(0, 1).reshape(S, H * dh)
+    ref_lse = (torch.logsumexp(logits, dim=-1) / np.log(2.0)).transpose(0, 1)  # log2 units
+    f = lambda t: t.detach().double().cpu().numpy()  # noqa: E731
+    close(f(out), f(ref), "bf16", "out")
+    assert np.abs(f(lse) - f(ref_lse)).max() <= 2e-2 * max(1.0, np.abs(f(ref_lse)).max())
