@@ -360,7 +360,7 @@ def run_sequence_parallel(args, rank, world, local, dist):
         hp = HL.build_halo_plan(ro, co, world)
         ex = SP.NcclExchange(None, rank, world, ctx=ctx)
         layer = HL.HaloAttention([hp[rank]], world, H, DH, args.dtype, HL.HaloNccl(ex, rank, ctx), ctx,
-                                 schedule=not args.no_schedule)
+                                 schedule=not args.no_schedule, overlap=False)
         rows = hp[rank].n_own
         halo_rows = [list(r.boundary_rows()) for r in hp]
     g = torch.Generator(device=dev).manual_seed(99 + rank)
@@ -382,18 +382,55 @@ def run_sequence_parallel(args, rank, world, local, dist):
         flush.zero_()
         step()
     torch.cuda.synchronize()
-    dist.barrier()
     n0 = ctx.launches
+    step()
+    torch.cuda.synchronize()
+    launches_per_step = ctx.launches - n0
+    # Mode H: the rank's whole step as one CUDA graph (NCCL send/recv included).
+    # Per GPU the step is ~40 small launches from Python; replaying them as one
+    # graph removes the host launch overhead that otherwise dominates once the
+    # per-GPU work is 1/N of the layer (profiles/r2w: 8 loopback ranks on one
+    # GPU 5.90 -> 2.47 ms). Every op of the halo path is on the current stream
+    # (HaloAttention with overlap=False); all ranks agree before using it.
+    graph, graph_out, graph_note = None, None, "eager (Ulysses mode)" if args.sp_mode == "ulysses" else "off"
+    if args.sp_mode == "halo" and not args.no_graph:
+        ok = 1
+        try:
+            side = torch.cuda.Stream(device=dev)
+            side.wait_stream(stream)
+            with torch.cuda.stream(side):
+                step()
+            stream.wait_stream(side)
+            torch.cuda.synchronize()
+            g_ = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g_):
+                graph_out = step()
+            torch.cuda.synchronize()
+            graph = g_
+        except Exception as exc:  # noqa: BLE001 - fall back to eager launches, reported in the line
+            ok, graph_note = 0, f"capture failed ({type(exc).__name__}); eager"
+        flag = torch.tensor([ok], device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 0:
+            graph = None
+            if ok:
+                graph_note = "capture failed on another rank; eager"
+        else:
+            graph_note = "one CUDA graph per rank per step"
+        ctx.set_stream(stream.cuda_stream)
+    run = graph.replay if graph is not None else step
+    torch.cuda.synchronize()
+    dist.barrier()
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         for i in range(args.steps):
             flush.zero_()
             evs[i][0].record(stream)
-            step()
+            run()
             evs[i][1].record(stream)
         torch.cuda.synchronize()
-    launches = ctx.launches - n0
+    launches = launches_per_step * args.steps
     ms = float(np.mean([a.elapsed_time(b) for a, b in evs]))
     t = torch.tensor([ms], device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -407,8 +444,14 @@ def run_sequence_parallel(args, rank, world, local, dist):
 
     def e2e_step():
         nonlocal hdb
-        dq_ = [x.to(dev, non_blocking=True) for x in (hq, hk, hv, hdo)]
-        o, (gq, gk, gv, gb) = step(tuple(dq_))
+        if graph is not None:  # host shards into the graph's input tensors, replay
+            for d_, h_ in ((q, hq), (k, hk), (v, hv), (do, hdo)):
+                d_.copy_(h_, non_blocking=True)
+            graph.replay()
+            o, (gq, gk, gv, gb) = graph_out
+        else:
+            dq_ = [x.to(dev, non_blocking=True) for x in (hq, hk, hv, hdo)]
+            o, (gq, gk, gv, gb) = step(tuple(dq_))
         if hdb is None:
             hdb = torch.empty(gb.shape, dtype=gb.dtype).pin_memory()
         for h_, d_ in ((ho, o[rank]), (hdq, gq[rank]), (hdk, gk[rank]), (hdv, gv[rank]), (hdb, gb)):
@@ -442,6 +485,7 @@ def run_sequence_parallel(args, rank, world, local, dist):
                                    + ("Ulysses head-split all-to-all" if args.sp_mode == "ulysses"
                                       else "cluster-halo exchange") + ")",
                        "sp_mode": args.sp_mode, "halo_rows_recv_sent_per_rank": halo_rows,
+                       "launch": graph_note,
                        "S": S, "E": int(E), "heads": H, "head_dim": DH, "pattern": args.pattern,
                        "parallelism": f"sp{world} ({args.sp_mode})",
                        "rows_per_gpu": rows, "a2a_bytes_sent_per_gpu_per_step": a2a,
@@ -477,6 +521,7 @@ def main():
                     help="run the ECR sub-blocks as dense tensor-core tiles (csrc/ecr_tile.cuh; measured slower at C3, "
                          "profiles/r2d)")
     ap.add_argument("--sp", action="store_true", help="run the sequence-parallel layer even at N = 1 (NCCL, 1 rank)")
+    ap.add_argument("--no-graph", action="store_true", help="N > 1 Mode H: launch the step eagerly (no CUDA graph)")
     ap.add_argument("--sp-mode", default="halo", choices=["halo", "ulysses"],
                     help="N > 1: cluster-halo row exchange (default) or the reference's Ulysses head split")
     ap.add_argument("--replicas", action="store_true",

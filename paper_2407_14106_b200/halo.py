@@ -19,10 +19,25 @@ rows its edges reach in other ranges:
             in rank order (gte_rows_scatter_add; unique rows per source, no
             atomics)
 
+Overlap (opt-in `overlap=True`): each rank's own rows split into *interior* rows
+(every column local) and *boundary* rows (some column in the halo), each with
+its own device plan over the same [own | halo] index space. The forward runs
+the interior rows while the K|V halo exchange is in flight on a second
+stream, then the boundary rows; the backward runs the boundary rows first
+(their dK|dV halo partials are complete then), sends those back on the
+second stream while the interior rows' backward runs, and adds the two
+plans' dQ / dK / dV (disjoint rows; own-column partial sums) before the
+owners' ordered scatter-add. Measured on the C3 pattern (profiles/r2w): the
+halo exchange is small (~10K rows of 2 x 128 B per rank at P = 8, a few us
+over NVLink) while the second plan per rank costs +30-60 % of the kernel
+time, so the default is one plan per rank; the step is then one stream of
+work that bench.py replays as a CUDA graph.
+
 The math per pair is the reference's (sparse_attention / _backward, the
 attention.cpp:96-320 semantics); only the summation order of dK/dV over
-ranks differs from a single GPU. The bias/dbias of a rank are the contiguous
-slice of the global pattern's edges that its rows own.
+ranks (and over the interior / boundary split) differs from a single GPU.
+The bias/dbias of a rank are the contiguous slice of the global pattern's
+edges that its rows own.
 """
 from __future__ import annotations
 
@@ -71,6 +86,15 @@ class RankHalo:
     local_co: np.ndarray
     e_lo: int                # own rows' edges are [e_lo, e_hi) of the global CSR
     e_hi: int
+    # interior / boundary split: the same CSR with only one kind of own row
+    # keeping its edges; eidx_* = those edges' positions in the local CSR
+    boundary: np.ndarray = None  # [n_ext] bool, own rows with a halo column
+    ro_i: np.ndarray = None
+    co_i: np.ndarray = None
+    eidx_i: np.ndarray = None
+    ro_b: np.ndarray = None
+    co_b: np.ndarray = None
+    eidx_b: np.ndarray = None
 
     @property
     def n_ext(self) -> int:
@@ -117,8 +141,28 @@ def build_halo_plan(row_offsets, cols, P: int) -> list[RankHalo]:
         lro = np.empty(n_ext + 1, dtype=np.int64)
         lro[: n_own + 1] = ro[lo:hi + 1] - e_lo
         lro[n_own + 1:] = e_hi - e_lo
-        plans.append(RankHalo(p, lo, hi, n_own, remote, recv_counts, send_idx, lro, lc, e_lo, e_hi))
+        r = RankHalo(p, lo, hi, n_own, remote, recv_counts, send_idx, lro, lc, e_lo, e_hi)
+        _split_rows(r)
+        plans.append(r)
     return plans
+
+
+def _split_rows(r: RankHalo) -> None:
+    """Interior / boundary sub-patterns of a rank's local CSR (same row space)."""
+    n_ext, ro, co = r.n_ext, r.local_ro, r.local_co
+    deg = np.diff(ro)
+    row_of = np.repeat(np.arange(n_ext), deg)
+    halo_edge = co >= r.n_own
+    boundary = np.zeros(n_ext, dtype=bool)
+    boundary[row_of[halo_edge]] = True
+    r.boundary = boundary
+    for tag, keep_rows in (("i", ~boundary), ("b", boundary)):
+        keep = keep_rows[row_of]
+        d = np.where(keep_rows, deg, 0)
+        sub_ro = np.concatenate([[0], np.cumsum(d)]).astype(np.int64)
+        setattr(r, "ro_" + tag, sub_ro)
+        setattr(r, "co_" + tag, co[keep])
+        setattr(r, "eidx_" + tag, np.nonzero(keep)[0].astype(np.int64))
 
 
 class HaloLoopback:
@@ -150,8 +194,11 @@ class HaloNccl:
         self.cx, self.rank, self.ctx = comm_exchange, rank, ctx
 
     def exchange(self, sends: dict, recvs: dict, send_counts: dict, recv_counts: dict, row_elems: int):
+        import torch
+
         p = self.rank
         x, y = sends[p], recvs[p]
+        self.ctx.set_stream(torch.cuda.current_stream().cuda_stream)  # the exchange stream under HaloAttention
         es = x.element_size() * row_elems
         sc = np.asarray(send_counts[p], dtype=np.int64) * es
         rc = np.asarray(recv_counts[p], dtype=np.int64) * es
@@ -184,59 +231,113 @@ class TorchDistHalo:
 
 class DeviceHaloOps:
     """The device half of HaloAttention: local plans + the sparse attention
-    kernels, row gather and ordered scatter-add (csrc/sp.cu)."""
+    kernels, row gather and ordered scatter-add (csrc/sp.cu), and a second
+    CUDA stream for the exchanges."""
 
     def __init__(self, heads: int, dh: int, dtype: str, ctx=None, schedule: bool = True):
         self.H, self.dh, self.dtype, self.d = heads, dh, dtype, heads * dh
         self.ctx = ctx or Context.get(0)
         self.schedule = schedule
         self.att = {}
+        self._comm = None
 
-    def setup(self, r: RankHalo):
-        plan = DevicePlan.from_host(r.local_ro, r.local_co, self.ctx)
+    def setup(self, key, n: int, ro: np.ndarray, co: np.ndarray):
+        plan = DevicePlan.from_host(ro, co, self.ctx)
         if self.schedule:
             plan.schedule()
-        self.att[r.rank] = DeviceSparseAttention(plan, self.H, self.dh, self.dh, self.dtype)
+        self.att[key] = DeviceSparseAttention(plan, self.H, self.dh, self.dh, self.dtype)
 
     def index(self, idx: np.ndarray):
         import torch
 
         return torch.tensor(idx.astype(np.int32), device=torch.device("cuda", self.ctx.device))
 
+    def _stream_here(self):
+        import torch
+
+        self.ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+
     def gather(self, ext, idx, n: int):
         import torch
 
         buf = torch.empty((max(n, 1), self.d), dtype=ext.dtype, device=ext.device)
         if n:
+            self._stream_here()
             check(_bind().gte_rows_gather(self.ctx.h, _lib.DTYPES[self.dtype], n, idx.data_ptr(), ext.data_ptr(),
                                           self.d, self.d, buf.data_ptr()))
         return buf
 
     def scatter_add(self, dst, idx, src, n: int):
+        self._stream_here()
         check(_bind().gte_rows_scatter_add(self.ctx.h, _lib.DTYPES[self.dtype], n, idx.data_ptr(), src.data_ptr(),
                                            self.d, dst.data_ptr(), self.d))
 
-    def attn_fwd(self, rank, q, k, v, b):
-        return self.att[rank].forward(q, k, v, b)
+    def attn_fwd(self, key, q, k, v, b):
+        return self.att[key].forward(q, k, v, b)
 
-    def attn_bwd(self, rank, q, k, v, o, lse, do, b):
-        return self.att[rank].backward(q, k, v, o, lse, do, b)
+    def attn_bwd(self, key, q, k, v, o, lse, do, b):
+        return self.att[key].backward(q, k, v, o, lse, do, b)
+
+    # ---- the exchange stream: work under `comm()` is ordered after the
+    # current stream's work so far; `join()` orders the current stream after it
+    def comm(self):
+        import torch
+
+        if self._comm is None:
+            self._comm = torch.cuda.Stream(device=torch.device("cuda", self.ctx.device))
+        self._comm.wait_stream(torch.cuda.current_stream())
+        return torch.cuda.stream(self._comm)
+
+    def join(self):
+        import torch
+
+        if self._comm is not None:
+            torch.cuda.current_stream().wait_stream(self._comm)
+
+
+class _Serial:
+    """Exchange "stream" of ops without one (CPU checkers): run in place."""
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
 
 
 class HaloAttention:
     """The sparse attention layer over P ranks with a cluster-halo exchange.
     `ranks` are the RankHalo plans this process holds (all P for the loopback,
     one for NCCL / torch.distributed). Shards: own rows [n_own, H*dh] per
-    rank. `ops` supplies the kernels (DeviceHaloOps unless given)."""
+    rank. `ops` supplies the kernels (DeviceHaloOps unless given). With
+    `overlap` the interior / boundary rows run on their own plans so the
+    exchanges overlap the interior rows' kernels (module docstring)."""
 
     def __init__(self, ranks: list[RankHalo], P: int, heads: int, dh: int, dtype: str, exchange, ctx=None,
-                 schedule: bool = True, ops=None):
+                 schedule: bool = True, ops=None, overlap: bool = False):
         self.ranks, self.P, self.H, self.dh, self.dtype, self.x = ranks, P, heads, dh, dtype, exchange
         self.d = heads * dh
         self.ops = ops or DeviceHaloOps(heads, dh, dtype, ctx, schedule)
+        self.overlap = overlap
+        import torch
+
+        dev = torch.device("cuda", self.ops.ctx.device) if hasattr(self.ops, "ctx") else torch.device("cpu")
         self.idx = {}
+        self.parts = {}  # rank -> [(tag, local edge positions)] of the plans that run
+        self._bmask = {}
         for r in ranks:
-            self.ops.setup(r)
+            if overlap and r.boundary is not None and r.n_ext > r.n_own:
+                parts = []
+                for tag in ("i", "b"):
+                    ro_, co_, ei = getattr(r, "ro_" + tag), getattr(r, "co_" + tag), getattr(r, "eidx_" + tag)
+                    if co_.shape[0]:
+                        self.ops.setup((r.rank, tag), r.n_ext, ro_, co_)
+                        parts.append((tag, torch.tensor(ei, dtype=torch.int64, device=dev)))
+                self.parts[r.rank] = parts
+                self._bmask[r.rank] = torch.tensor(r.boundary, device=dev)
+            else:
+                self.ops.setup((r.rank, "all"), r.n_ext, r.local_ro, r.local_co)
+                self.parts[r.rank] = [("all", None)]
             cat = np.concatenate(r.send_idx) if r.send_idx else np.zeros(0, np.int32)
             self.idx[r.rank] = self.ops.index(cat)
         self._send_counts = {r.rank: [len(s) for s in r.send_idx] for r in ranks}
@@ -247,11 +348,19 @@ class HaloAttention:
         self.cache = {}
         self._bufs = {}
 
+    def _comm(self):
+        return self.ops.comm() if hasattr(self.ops, "comm") else _Serial()
+
+    def _join(self):
+        if hasattr(self.ops, "join"):
+            self.ops.join()
+
     def _ext(self, r: RankHalo, own, name: str, zero_tail: bool = False):
         """[own | halo] buffer, persistent per (rank, tensor): allocated once,
-        own rows copied in each step. Tails that no exchange fills (Q, dO) are
-        zeroed once: the kernels' padding slots may read any row of the local
-        index space."""
+        own rows copied in each step. Tails are zeroed once: the kernels'
+        padding slots may read any row of the local index space, and with the
+        overlap the interior plan's own-row checks read the K / V tails while
+        the exchange rewrites them (always finite values)."""
         if r.n_ext == r.n_own:
             return own.contiguous()
         key = (r.rank, name)
@@ -286,10 +395,9 @@ class HaloAttention:
                 kx[r.rank][r.n_own:].copy_(recvs[r.rank][:m, : self.d])
                 vx[r.rank][r.n_own:].copy_(recvs[r.rank][:m, self.d:])
 
-    def _halo_back_kv(self, gk: dict, gv: dict):
+    def _halo_back_send(self, gk: dict, gv: dict) -> dict:
         """Send the halo rows' dK | dV partial sums to their owners in one
-        all_to_allv and add them to the owners' rows, source by source in
-        rank order (unique rows per source: no atomics, fixed order)."""
+        all_to_allv; returns the received blocks per rank."""
         import torch
 
         sends, recvs = {}, {}
@@ -302,6 +410,11 @@ class HaloAttention:
                 sends[r.rank] = gk[r.rank].new_zeros((1, 2 * self.d))
             recvs[r.rank] = gk[r.rank].new_empty((max(n, 1), 2 * self.d))
         self.x.exchange(sends, recvs, self._all_recv_counts(), self._all_send_counts(), 2 * self.d)
+        return recvs
+
+    def _halo_back_add(self, gk: dict, gv: dict, recvs: dict):
+        """Add the received partials to the owners' rows, source by source in
+        rank order (unique rows per source: no atomics, fixed order)."""
         for r in self.ranks:
             off = 0
             idx, rv = self.idx[r.rank], recvs[r.rank]
@@ -318,28 +431,98 @@ class HaloAttention:
     def _all_recv_counts(self):
         return getattr(self, "_all_recv", self._recv_counts)
 
+    @staticmethod
+    def _take(b, ei):
+        return None if b is None or ei is None else b[ei]
+
+    def _merge_rows(self, r: RankHalo, a, b):
+        """Rows of the boundary plan's result over the interior plan's."""
+        if a is None or b is None:
+            return a if b is None else b
+        m = self._bmask[r.rank]
+        return a.where(~m.view(-1, *([1] * (a.dim() - 1))), b)
+
     def forward(self, q: dict, k: dict, v: dict, bias=None):
         """bias: the global pattern's [E] (each rank uses its edges' slice)."""
-        kx = {r.rank: self._ext(r, k[r.rank], "k") for r in self.ranks}
-        vx = {r.rank: self._ext(r, v[r.rank], "v") for r in self.ranks}
-        self._halo_in_kv(kx, vx)
+        kx = {r.rank: self._ext(r, k[r.rank], "k", zero_tail=True) for r in self.ranks}
+        vx = {r.rank: self._ext(r, v[r.rank], "v", zero_tail=True) for r in self.ranks}
+        qx = {r.rank: self._ext(r, q[r.rank], "q", zero_tail=True) for r in self.ranks}
+        bl = {r.rank: None if bias is None else bias[r.e_lo:r.e_hi] for r in self.ranks}
+        res = {r.rank: {} for r in self.ranks}
+        with self._comm():  # halo rows in, on the exchange stream
+            self._halo_in_kv(kx, vx)
+        for r in self.ranks:  # interior rows (no halo column) meanwhile
+            for tag, ei in self.parts[r.rank]:
+                if tag == "i":
+                    res[r.rank][tag] = self.ops.attn_fwd((r.rank, tag), qx[r.rank], kx[r.rank], vx[r.rank],
+                                                         self._take(bl[r.rank], ei))
+        self._join()
         out = {}
         for r in self.ranks:
-            qx = self._ext(r, q[r.rank], "q", zero_tail=True)
-            b = None if bias is None else bias[r.e_lo:r.e_hi]
-            o, lse = self.ops.attn_fwd(r.rank, qx, kx[r.rank], vx[r.rank], b)
-            self.cache[r.rank] = (qx, kx[r.rank], vx[r.rank], o, lse, b)
+            for tag, ei in self.parts[r.rank]:
+                if tag != "i":
+                    b = bl[r.rank] if tag == "all" else self._take(bl[r.rank], ei)
+                    res[r.rank][tag] = self.ops.attn_fwd((r.rank, tag), qx[r.rank], kx[r.rank], vx[r.rank], b)
+            got = res[r.rank]
+            if "all" in got:
+                o, lse = got["all"]
+            else:
+                oi, li = got.get("i", (None, None))
+                ob, lb = got.get("b", (None, None))
+                o, lse = self._merge_rows(r, oi, ob), self._merge_rows(r, li, lb)
+            self.cache[r.rank] = (qx[r.rank], kx[r.rank], vx[r.rank], o, lse, bl[r.rank])
             out[r.rank] = o[: r.n_own]
         return out
 
     def backward(self, dout: dict):
         """Returns {rank: (dq_own, dk_own, dv_own, dbias_own_edges)}."""
+        import torch
+
+        got, dox = {}, {}
+        for r in self.ranks:  # boundary rows first: the halo partials are complete after them
+            qx, kx, vx, o, lse, b = self.cache[r.rank]
+            dox[r.rank] = self._ext(r, dout[r.rank], "do", zero_tail=True)
+            got[r.rank] = {}
+            for tag, ei in self.parts[r.rank]:
+                if tag != "i":
+                    bb = b if tag == "all" else self._take(b, ei)
+                    got[r.rank][tag] = self.ops.attn_bwd((r.rank, tag), qx, kx, vx, o, lse, dox[r.rank], bb)
+        first = {r.rank: next(iter(got[r.rank].values())) if got[r.rank] else None for r in self.ranks}
+        send_k = {p: (g[1] if g is not None else None) for p, g in first.items()}
+        send_v = {p: (g[2] if g is not None else None) for p, g in first.items()}
+        for r in self.ranks:  # a rank without boundary rows sends zeros
+            if send_k[r.rank] is None:
+                qx = self.cache[r.rank][0]
+                send_k[r.rank] = qx.new_zeros((r.n_ext, self.d))
+                send_v[r.rank] = qx.new_zeros((r.n_ext, self.d))
+        with self._comm():  # halo dK | dV partials back, on the exchange stream
+            recvs = self._halo_back_send(send_k, send_v)
+        for r in self.ranks:  # interior rows meanwhile
+            qx, kx, vx, o, lse, b = self.cache[r.rank]
+            for tag, ei in self.parts[r.rank]:
+                if tag == "i":
+                    got[r.rank][tag] = self.ops.attn_bwd((r.rank, tag), qx, kx, vx, o, lse, dox[r.rank],
+                                                         self._take(b, ei))
         gq, gk, gv, gb = {}, {}, {}, {}
         for r in self.ranks:
-            qx, kx, vx, o, lse, b = self.cache[r.rank]
-            dox = self._ext(r, dout[r.rank], "do", zero_tail=True)
-            dq, dk, dv, db = self.ops.attn_bwd(r.rank, qx, kx, vx, o, lse, dox, b)
+            parts = got[r.rank]
+            if "all" in parts:
+                gq[r.rank], gk[r.rank], gv[r.rank], gb[r.rank] = parts["all"]
+                continue
+            dq = dk = dv = None
+            db = None
+            for tag, ei in self.parts[r.rank]:
+                a_q, a_k, a_v, a_b = parts[tag]
+                # disjoint rows for dQ; own-column partial sums for dK / dV
+                dq = a_q if dq is None else dq + a_q
+                dk = a_k if dk is None else dk + a_k
+                dv = a_v if dv is None else dv + a_v
+                if a_b is not None:
+                    if db is None:
+                        db = a_b.new_zeros(r.e_hi - r.e_lo)
+                    db[ei] = a_b[: ei.shape[0]]
             gq[r.rank], gk[r.rank], gv[r.rank], gb[r.rank] = dq, dk, dv, db
-        self._halo_back_kv(gk, gv)
+        self._join()
+        self._halo_back_add(gk, gv, recvs)
         return {r.rank: (gq[r.rank][: r.n_own], gk[r.rank][: r.n_own], gv[r.rank][: r.n_own],
                          gb[r.rank][: r.e_hi - r.e_lo]) for r in self.ranks}

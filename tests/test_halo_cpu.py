@@ -97,10 +97,10 @@ class CpuHaloOps:
     def __init__(self, orc, H, dh):
         self.orc, self.H, self.dh, self.g = orc, H, dh, {}
 
-    def setup(self, r):
+    def setup(self, key, n, ro, co):
         from oracle import CSR
 
-        self.g[r.rank] = CSR(r.n_ext, r.local_ro, r.local_co)
+        self.g[key] = CSR(n, ro, co)
 
     def index(self, idx):
         import torch
@@ -116,23 +116,23 @@ class CpuHaloOps:
     def _heads(self, x, h):
         return x[:, h * self.dh:(h + 1) * self.dh].numpy()
 
-    def attn_fwd(self, rank, q, k, v, b):
+    def attn_fwd(self, key, q, k, v, b):
         import torch
 
         o = np.zeros(q.shape)
         for h in range(self.H):
             o[:, h * self.dh:(h + 1) * self.dh] = self.orc.sparse_fwd(
-                self._heads(q, h), self._heads(k, h), self._heads(v, h), self.g[rank], None if b is None else b.numpy())
+                self._heads(q, h), self._heads(k, h), self._heads(v, h), self.g[key], None if b is None else b.numpy())
         return torch.tensor(o), None
 
-    def attn_bwd(self, rank, q, k, v, o, lse, do, b):
+    def attn_bwd(self, key, q, k, v, o, lse, do, b):
         import torch
 
         dq, dk, dv = (np.zeros(q.shape) for _ in range(3))
-        db = np.zeros(self.g[rank].nnz)
+        db = np.zeros(self.g[key].nnz)
         for h in range(self.H):
             sl = slice(h * self.dh, (h + 1) * self.dh)
-            a, c, e, f = self.orc.sparse_bwd(self._heads(q, h), self._heads(k, h), self._heads(v, h), self.g[rank],
+            a, c, e, f = self.orc.sparse_bwd(self._heads(q, h), self._heads(k, h), self._heads(v, h), self.g[key],
                                              None if b is None else b.numpy(), None, self._heads(do, h))
             dq[:, sl], dk[:, sl], dv[:, sl] = a, c, e
             db += f
@@ -210,3 +210,58 @@ def test_gloo_ranks_halo_protocol_matches_oracle(orc, tmp_path, world):
             assert np.abs(got[n][:, sl] - w).max() < 1e-12, n
         dbw += e
     assert np.abs(db - dbw).max() < 1e-12
+
+
+@pytest.mark.parametrize("P", [2, 3, 8])
+def test_interior_boundary_split_partitions_local_csr(P):
+    """The overlap's two sub-plans: boundary rows are exactly the own rows with
+    a halo column; each sub-CSR keeps its rows' edges in local order and the
+    two edge position lists partition the local CSR."""
+    ro, co = community_graph(3000, 9.0, community=64, seed=P, shuffle=True)
+    for r in build_halo_plan(ro, co, P):
+        want_b = np.zeros(r.n_ext, dtype=bool)
+        for i in range(r.n_own):
+            want_b[i] = np.any(r.local_co[r.local_ro[i]:r.local_ro[i + 1]] >= r.n_own)
+        assert np.array_equal(r.boundary, want_b)
+        both = np.sort(np.concatenate([r.eidx_i, r.eidx_b]))
+        assert np.array_equal(both, np.arange(r.local_co.shape[0]))
+        for tag, rows in (("i", ~r.boundary), ("b", r.boundary)):
+            sro, sco, ei = getattr(r, "ro_" + tag), getattr(r, "co_" + tag), getattr(r, "eidx_" + tag)
+            assert sro.shape[0] == r.n_ext + 1 and sro[-1] == sco.shape[0] == ei.shape[0]
+            assert np.array_equal(sco, r.local_co[ei])
+            for i in range(r.n_ext):
+                n = sro[i + 1] - sro[i]
+                assert n == (r.local_ro[i + 1] - r.local_ro[i] if rows[i] else 0)
+        assert np.all(r.co_i < r.n_own)  # interior rows never touch the halo
+
+
+def test_overlapped_protocol_matches_serial(orc):
+    """HaloAttention with the interior / boundary split (overlap) against the
+    single-plan protocol, 3 logical ranks in one process with the oracle as
+    the kernel (f64): outputs, dQ, dK, dV and dbias agree to 1e-12."""
+    import torch
+
+    from oracle import Oracle
+
+    from paper_2407_14106_b200.halo import HaloAttention, HaloLoopback
+
+    P, H, dh = 3, 2, 4
+    ro, co = community_graph(900, 7.0, community=50, seed=5, shuffle=True)
+    S = ro.shape[0] - 1
+    rng = np.random.default_rng(1)
+    q, k, v, up = (torch.tensor(rng.standard_normal((S, H * dh))) for _ in range(4))
+    bias = torch.tensor(rng.normal(0, 0.3, co.shape[0]))
+    plans = build_halo_plan(ro, co, P)
+    assert all(r.boundary[: r.n_own].any() and (~r.boundary[: r.n_own]).any() for r in plans)
+    res = {}
+    for overlap in (False, True):
+        layer = HaloAttention(plans, P, H, dh, "f64", HaloLoopback(P), ops=CpuHaloOps(Oracle(), H, dh),
+                              overlap=overlap)
+        sl = lambda t, r: t[r.lo:r.hi].clone()  # noqa: E731
+        out = layer.forward({r.rank: sl(q, r) for r in plans}, {r.rank: sl(k, r) for r in plans},
+                            {r.rank: sl(v, r) for r in plans}, bias)
+        grads = layer.backward({r.rank: sl(up, r) for r in plans})
+        res[overlap] = [torch.cat([out[r.rank] for r in plans]).numpy()] + [
+            torch.cat([grads[r.rank][j] for r in plans]).numpy() for j in range(4)]
+    for a, b in zip(res[False], res[True]):
+        assert np.abs(a - b).max() <= 1e-12 * max(1.0, np.abs(a).max())

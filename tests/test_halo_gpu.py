@@ -17,7 +17,7 @@ pytestmark = pytest.mark.gpu
 TOL = {"f64": 1e-12, "f32": 1e-5, "bf16": 1e-2}
 
 
-def _run(ro, co, P, H, dh, dtype, seed=0):
+def _run(ro, co, P, H, dh, dtype, seed=0, overlap=False):
     import torch
 
     td = {"f64": torch.float64, "f32": torch.float32, "bf16": torch.bfloat16}[dtype]
@@ -27,7 +27,7 @@ def _run(ro, co, P, H, dh, dtype, seed=0):
     q, k, v, up = (torch.randn((S, H * dh), generator=g, device="cuda").to(td) for _ in range(4))
     bias = (0.3 * torch.randn(E, generator=g, device="cuda")).to(acc)
     plans = build_halo_plan(ro, co, P)
-    layer = HaloAttention(plans, P, H, dh, dtype, HaloLoopback(P))
+    layer = HaloAttention(plans, P, H, dh, dtype, HaloLoopback(P), overlap=overlap)
     sl = lambda t, r: t[r.lo:r.hi].contiguous()  # noqa: E731
     out = layer.forward({r.rank: sl(q, r) for r in plans}, {r.rank: sl(k, r) for r in plans},
                         {r.rank: sl(v, r) for r in plans}, bias)
@@ -48,11 +48,14 @@ def _run(ro, co, P, H, dh, dtype, seed=0):
     return res, one, inputs, plans
 
 
+@pytest.mark.parametrize("overlap", [False, True])
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
 @pytest.mark.parametrize("P", [2, 4, 8])
-def test_halo_matches_single_gpu(cuda, dtype, P):
+def test_halo_matches_single_gpu(cuda, dtype, P, overlap):
+    """P logical ranks on one GPU against the single-GPU layer; with
+    `overlap` the interior / boundary plans and the exchange stream."""
     ro, co = community_graph(20000, 12.0, community=256, seed=P, shuffle=False)
-    res, one, _, plans = _run(ro, co, P, 8, 8, dtype, seed=P)
+    res, one, _, plans = _run(ro, co, P, 8, 8, dtype, seed=P, overlap=overlap)
     for nm in ("out", "dq", "dk", "dv", "db"):
         e = rel_err(res[nm], one[nm])
         assert max(e) <= TOL[dtype], (nm, e)
@@ -102,3 +105,43 @@ def test_all_to_allv_single_rank(cuda):
     torch.cuda.synchronize()
     assert torch.equal(x, y)
     nx.close()
+
+
+@pytest.mark.parametrize("overlap", [False, True])
+def test_halo_step_graph_capture_matches_eager(cuda, overlap):
+    """The Mode H step captured as one CUDA graph (what bench.py replays per
+    rank) gives the eager step's results bit for bit: every op of the path is
+    stream-ordered on the capturing stream (or forked / joined from it)."""
+    import torch
+
+    P, H, dh = 4, 8, 8
+    ro, co = community_graph(12000, 10.0, community=256, seed=11, shuffle=False)
+    S, E = ro.shape[0] - 1, co.shape[0]
+    g = torch.Generator(device="cuda").manual_seed(5)
+    q, k, v, up = (torch.randn((S, H * dh), generator=g, device="cuda").to(torch.bfloat16) for _ in range(4))
+    bias = (0.3 * torch.randn(E, generator=g, device="cuda")).float()
+    plans = build_halo_plan(ro, co, P)
+    layer = HaloAttention(plans, P, H, dh, "bf16", HaloLoopback(P), overlap=overlap)
+    sl = lambda t, r: t[r.lo:r.hi]  # noqa: E731
+
+    def step():
+        o = layer.forward({r.rank: sl(q, r) for r in plans}, {r.rank: sl(k, r) for r in plans},
+                          {r.rank: sl(v, r) for r in plans}, bias)
+        gr = layer.backward({r.rank: sl(up, r) for r in plans})
+        return [o[r.rank] for r in plans] + [x for r in plans for x in gr[r.rank]]
+
+    eager = [x.clone() for x in step()]
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        step()
+    torch.cuda.current_stream().wait_stream(side)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        out = step()
+    for t_ in out:
+        t_.zero_()
+    graph.replay()
+    torch.cuda.synchronize()
+    for a_, b_ in zip(eager, out):
+        assert torch.equal(a_, b_)
