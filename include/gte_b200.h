@@ -445,6 +445,13 @@ int gte_rows_gather(gte_ctx* ctx, int dtype, int64_t n, const int32_t* idx, cons
                     void* dst);
 int gte_rows_scatter_add(gte_ctx* ctx, int dtype, int64_t n, const int32_t* idx, const void* src, int64_t w,
                          void* dst, int64_t ld);
+/* All peers' partials in one launch: for u < n_rows, row rows[u] of dst gets
+ * src rows pos[ptr[u]], pos[ptr[u] + 1], ... added one after the other, in
+ * that order (the order of the per-peer gte_rows_scatter_add calls it
+ * replaces, with the same per-add rounding: bit-identical). src rows are
+ * ld_src apart, dst rows ld apart, w elements each. */
+int gte_rows_scatter_add_seq(gte_ctx* ctx, int dtype, int64_t n_rows, const int32_t* rows, const int32_t* ptr,
+                             const int32_t* pos, const void* src, int64_t ld_src, int64_t w, void* dst, int64_t ld);
 
 #ifdef __cplusplus
 }

@@ -203,6 +203,22 @@ __global__ void scatter_add_rows_kernel(const T* __restrict__ src, const int32_t
   }
 }
 
+// dst[rows[u]][c] += src[pos[j]][c] for j in [ptr[u], ptr[u+1]), in j order,
+// rounding to T after every add (as the per-source kernel above does)
+template <typename T, typename A>
+__global__ void scatter_add_seq_kernel(const T* __restrict__ src, int64_t lds, const int32_t* __restrict__ rows,
+                                       const int32_t* __restrict__ ptr, const int32_t* __restrict__ pos, int64_t n,
+                                       int64_t w, T* __restrict__ dst, int64_t ld) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n * w; x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t u = x / w, c = x % w;
+    T* d = dst + (int64_t)__ldg(rows + u) * ld + c;
+    T acc = *d;
+    for (int j = __ldg(ptr + u), j1 = __ldg(ptr + u + 1); j < j1; ++j)
+      acc = T(A(acc) + A(src[(int64_t)__ldg(pos + j) * lds + c]));
+    *d = acc;
+  }
+}
+
 int unit_bytes(int64_t chunk_row_bytes, std::initializer_list<const void*> ptrs) {
   for (int u : {16, 8, 4, 2, 1}) {
     if (chunk_row_bytes % u) continue;
@@ -405,6 +421,31 @@ int gte_rows_scatter_add(gte_ctx* ctx, int dtype, int64_t n, const int32_t* idx,
     default:
       scatter_add_rows_kernel<__nv_bfloat16, float><<<g, 256, 0, st>>>((const __nv_bfloat16*)src, idx, n, w,
                                                                         (__nv_bfloat16*)dst, ld);
+      break;
+  }
+  ctx_launch_counter(ctx) += 1;
+  SCUDA(cudaGetLastError());
+  return GTE_OK;
+}
+
+int gte_rows_scatter_add_seq(gte_ctx* ctx, int dtype, int64_t n, const int32_t* rows, const int32_t* ptr,
+                             const int32_t* pos, const void* src, int64_t lds, int64_t w, void* dst, int64_t ld) {
+  if (n < 0 || w < 0 || ld < w || lds < w) return set_error(GTE_CONFIG, "rows_scatter_add_seq: bad sizes");
+  if (n == 0 || w == 0) return GTE_OK;
+  cudaStream_t st = (cudaStream_t)ctx_stream(ctx);
+  const unsigned g = blocks_for(n * w);
+  switch (dtype) {
+    case GTE_F64:
+      scatter_add_seq_kernel<double, double><<<g, 256, 0, st>>>((const double*)src, lds, rows, ptr, pos, n, w,
+                                                                 (double*)dst, ld);
+      break;
+    case GTE_F32:
+      scatter_add_seq_kernel<float, float><<<g, 256, 0, st>>>((const float*)src, lds, rows, ptr, pos, n, w,
+                                                               (float*)dst, ld);
+      break;
+    default:
+      scatter_add_seq_kernel<__nv_bfloat16, float><<<g, 256, 0, st>>>((const __nv_bfloat16*)src, lds, rows, ptr, pos,
+                                                                       n, w, (__nv_bfloat16*)dst, ld);
       break;
   }
   ctx_launch_counter(ctx) += 1;

@@ -59,6 +59,7 @@ def _bind():
         L.gte_rows_gather.argtypes = [VP, I32, I64, VP, VP, I64, I64, VP]
         L.gte_rows_scatter_add.argtypes = [VP, I32, I64, VP, VP, I64, VP, I64]
         L.gte_comm_all_to_allv.argtypes = [VP, VP, VP, VP, VP, VP, VP, VP]
+        L.gte_rows_scatter_add_seq.argtypes = [VP, I32, I64, VP, VP, VP, VP, I64, I64, VP, I64]
         L._halo_bound = True
     return L
 
@@ -272,6 +273,18 @@ class DeviceHaloOps:
         check(_bind().gte_rows_scatter_add(self.ctx.h, _lib.DTYPES[self.dtype], n, idx.data_ptr(), src.data_ptr(),
                                            self.d, dst.data_ptr(), self.d))
 
+    def scatter_add_seq(self, dst, seq, src, col0: int):
+        """dst[rows[u]] += src[pos[j], col0:col0+d] for j in [ptr[u], ptr[u+1])
+        in order: every peer's partials in one launch (gte_rows_scatter_add_seq)."""
+        rows, ptr, pos = seq
+        n = int(rows.numel())
+        if n:
+            self._stream_here()
+            check(_bind().gte_rows_scatter_add_seq(self.ctx.h, _lib.DTYPES[self.dtype], n, rows.data_ptr(),
+                                                   ptr.data_ptr(), pos.data_ptr(),
+                                                   src.data_ptr() + col0 * src.element_size(), src.stride(0),
+                                                   self.d, dst.data_ptr(), dst.stride(0)))
+
     def attn_fwd(self, key, q, k, v, b):
         return self.att[key].forward(q, k, v, b)
 
@@ -325,6 +338,7 @@ class HaloAttention:
         self.idx = {}
         self.parts = {}  # rank -> [(tag, local edge positions)] of the plans that run
         self._bmask = {}
+        self._seq = {}
         for r in ranks:
             if overlap and r.boundary is not None and r.n_ext > r.n_own:
                 parts = []
@@ -340,6 +354,11 @@ class HaloAttention:
                 self.parts[r.rank] = [("all", None)]
             cat = np.concatenate(r.send_idx) if r.send_idx else np.zeros(0, np.int32)
             self.idx[r.rank] = self.ops.index(cat)
+            if hasattr(self.ops, "scatter_add_seq"):  # the peers' partials per own row, in peer order
+                order = np.argsort(cat, kind="stable")
+                rows_u, first, cnt = np.unique(cat[order], return_index=True, return_counts=True)
+                ptr = np.concatenate([[0], np.cumsum(cnt)])
+                self._seq[r.rank] = tuple(self.ops.index(x) for x in (rows_u, ptr, order))
         self._send_counts = {r.rank: [len(s) for s in r.send_idx] for r in ranks}
         self._recv_counts = {r.rank: list(r.recv_counts) for r in ranks}
         if len(ranks) == P:  # loopback: every rank's counts are local
@@ -414,8 +433,13 @@ class HaloAttention:
 
     def _halo_back_add(self, gk: dict, gv: dict, recvs: dict):
         """Add the received partials to the owners' rows, source by source in
-        rank order (unique rows per source: no atomics, fixed order)."""
+        rank order (unique rows per source: no atomics, fixed order) — on the
+        device as one ordered launch per tensor."""
         for r in self.ranks:
+            if r.rank in self._seq:
+                self.ops.scatter_add_seq(gk[r.rank], self._seq[r.rank], recvs[r.rank], 0)
+                self.ops.scatter_add_seq(gv[r.rank], self._seq[r.rank], recvs[r.rank], self.d)
+                continue
             off = 0
             idx, rv = self.idx[r.rank], recvs[r.rank]
             for n in self._send_counts[r.rank]:
