@@ -775,6 +775,9 @@ __global__ void __launch_bounds__(kBT, 2)
     stage_tl<DVP>(&tmV, a.v, a.ldv, h, a.dv, c, nn, base + kN * DKP * 2, nullptr, 0, kBT);
   };
   uint32_t phase = 0;
+  float g[kHK];  // this thread's half of its dQ row, summed over key blocks in registers
+#pragma unroll
+  for (int t = 0; t < kHK; ++t) g[t] = 0.f;
   const bool rows_full = r0 + kM <= a.s_real;  // CTA-uniform
   const uint64_t sc2 = pk2(a.scale_l, a.scale_l), nl2 = pk2(-lse, -lse), nd2 = pk2(-delta, -delta);
   if (a.s_real > 0) stage_keys(0, 0);
@@ -789,9 +792,12 @@ __global__ void __launch_bounds__(kBT, 2)
     __syncthreads();
     tc_after_sync();
     if (c0 + kN < a.s_real) stage_keys(c0 + kN, buf ^ 1);  // the other buffer's MMAs completed last block
-    if (tid == 0) {  // S = Q K^T
+    if (tid == 0) {  // S = Q K^T -> columns [0, 128), dP = dO V^T -> [128, 256): independent, one commit
 #pragma unroll
       for (int kc = 0; kc < DKP / 16; ++kc) mma_bf16(tmem, kdesc(sQ, kc), kdesc(sK, kc), instr_desc(kM, kN), kc > 0);
+#pragma unroll
+      for (int kc = 0; kc < DVP / 16; ++kc)
+        mma_bf16(tmem + 128, kdesc(sD, kc), kdesc(sV, kc), instr_desc(kM, kN), kc > 0);
       mma_commit(bar);
     }
     mbar_wait(bar, phase);
@@ -821,21 +827,10 @@ __global__ void __launch_bounds__(kBT, 2)
         p[q4 * 16 + i] = (real && c < n) ? ex2_approx(x) : 0.f;
       }
     }
-    tc_before_sync();
-    __syncthreads();
-    tc_after_sync();
-    if (tid == 0) {  // dP = dO V^T (same TMEM columns; S is in registers)
-#pragma unroll
-      for (int kc = 0; kc < DVP / 16; ++kc) mma_bf16(tmem, kdesc(sD, kc), kdesc(sV, kc), instr_desc(kM, kN), kc > 0);
-      mma_commit(bar);
-    }
-    mbar_wait(bar, phase);
-    phase ^= 1;
-    tc_after_sync();
 #pragma unroll
     for (int q4 = 0; q4 < kHN / 16; ++q4) {
       float v16[16];
-      tmem_ld16(t_row + cb + q4 * 16, v16);
+      tmem_ld16(t_row + 128 + cb + q4 * 16, v16);
 #pragma unroll
       for (int c8 = 0; c8 < 2; ++c8) {
         uint32_t w[4];
@@ -853,22 +848,23 @@ __global__ void __launch_bounds__(kBT, 2)
     tc_before_sync();
     __syncthreads();
     tc_after_sync();
-    if (tid == 0) {  // dQ += dS K  (A = dS K-major, B = K MN-major, N = DKP)
+    if (tid == 0) {  // dQ_blk = dS K into the consumed S columns (A = dS K-major, B = K MN-major, N = DKP)
 #pragma unroll
       for (int kc = 0; kc < kN / 16; ++kc)
-        mma_bf16(tmem + 128, smem_desc(sS + kc * 256, 128, kN * 16), mndesc(sK, kc), instr_desc_bmn(kM, DKP),
-                 (c0 > 0 || kc > 0) ? 1u : 0u);
+        mma_bf16(tmem, smem_desc(sS + kc * 256, 128, kN * 16), mndesc(sK, kc), instr_desc_bmn(kM, DKP), kc > 0);
       mma_commit(bar);
     }
     mbar_wait(bar, phase);
     phase ^= 1;
     tc_after_sync();
-  }
-  // tcgen05.ld is warp-collective: every thread loads, only valid rows store
-  float g[kHK];
+    {
+      float gb[kHK];
+      tmem_ld_cols<kHK>(t_row + half * kHK, gb);
 #pragma unroll
-  for (int t = 0; t < kHK; ++t) g[t] = 0.f;
-  if (a.s_real > 0) tmem_ld_cols<kHK>(t_row + 128 + half * kHK, g);
+      for (int t = 0; t < kHK; ++t) g[t] += gb[t];
+    }
+  }
+  // tcgen05.ld is warp-collective: every thread loaded, only valid rows store
   if (row < a.S) {
 #pragma unroll
     for (int t = 0; t < kHK; ++t) {
@@ -930,7 +926,7 @@ __global__ void __launch_bounds__(kBT, 2)
   const uint32_t sK = (uint32_t)__cvta_generic_to_shared(Ks), sV = (uint32_t)__cvta_generic_to_shared(Vs);
   const uint32_t sQB = (uint32_t)__cvta_generic_to_shared(QB);
   const uint32_t sPt = (uint32_t)__cvta_generic_to_shared(Pt), sSt = (uint32_t)__cvta_generic_to_shared(St);
-  constexpr uint32_t kColV = 128, kColK = 192;  // dV, dK accumulators
+  constexpr uint32_t kColV = 0, kColK = DVP;  // dV_blk, dK_blk (registers accumulate them)
   constexpr int oDk = kN * DKP * 2, oLs = oDk + kN * DVP * 2;
   auto stage_queries = [&](int64_t q, int b) {
     const int nn = (int)(a.s_real - q < kN ? a.s_real - q : kN);
@@ -956,6 +952,11 @@ __global__ void __launch_bounds__(kBT, 2)
     cp_async_commit();
   };
   uint32_t phase = 0;
+  float gv[kHV], gk[kHK];  // this thread's halves of its dV / dK rows, summed over query blocks in registers
+#pragma unroll
+  for (int t = 0; t < kHV; ++t) gv[t] = 0.f;
+#pragma unroll
+  for (int t = 0; t < kHK; ++t) gk[t] = 0.f;
   const bool keys_full = k0 + kM <= a.s_real;  // CTA-uniform
   if (a.s_real > 0) stage_queries(0, 0);
   int buf = 0;
@@ -972,10 +973,13 @@ __global__ void __launch_bounds__(kBT, 2)
     __syncthreads();
     tc_after_sync();
     if (q0 + kN < a.s_real) stage_queries(q0 + kN, buf ^ 1);  // the other buffer's MMAs completed last block
-    if (tid == 0) {  // S^T = K Q^T
+    if (tid == 0) {  // S^T = K Q^T -> columns [0, 128), dP^T = V dO^T -> [128, 256): one commit
 #pragma unroll
       for (int kc = 0; kc < DKP / 16; ++kc)
         mma_bf16(tmem, kdesc(sK, kc), kdesc(sQk, kc), instr_desc(kM, kN), kc > 0);
+#pragma unroll
+      for (int kc = 0; kc < DVP / 16; ++kc)
+        mma_bf16(tmem + 128, kdesc(sV, kc), kdesc(sDk, kc), instr_desc(kM, kN), kc > 0);
       mma_commit(bar);
     }
     mbar_wait(bar, phase);
@@ -1019,22 +1023,10 @@ __global__ void __launch_bounds__(kBT, 2)
         *reinterpret_cast<uint4*>(Pt + canon(rl, cb + q4 * 16 + c8 * 8, kN)) = make_uint4(w[0], w[1], w[2], w[3]);
       }
     }
-    tc_before_sync();
-    __syncthreads();
-    tc_after_sync();
-    if (tid == 0) {  // dP^T = V dO^T
-#pragma unroll
-      for (int kc = 0; kc < DVP / 16; ++kc)
-        mma_bf16(tmem, kdesc(sV, kc), kdesc(sDk, kc), instr_desc(kM, kN), kc > 0);
-      mma_commit(bar);
-    }
-    mbar_wait(bar, phase);
-    phase ^= 1;
-    tc_after_sync();
 #pragma unroll
     for (int q4 = 0; q4 < kHN / 16; ++q4) {
       float v16[16];
-      tmem_ld16(t_row + cb + q4 * 16, v16);
+      tmem_ld16(t_row + 128 + cb + q4 * 16, v16);
 #pragma unroll
       for (int c8 = 0; c8 < 2; ++c8) {
         uint32_t w[4];
@@ -1053,32 +1045,31 @@ __global__ void __launch_bounds__(kBT, 2)
     tc_before_sync();
     __syncthreads();
     tc_after_sync();
-    if (tid == 0) {  // dV += P^T dO, dK += dS^T Q
+    if (tid == 0) {  // dV_blk = P^T dO, dK_blk = dS^T Q into the consumed S^T columns
 #pragma unroll
       for (int kc = 0; kc < kN / 16; ++kc)
         mma_bf16(tmem + kColV, smem_desc(sPt + kc * 256, 128, kN * 16), mndesc(sDk, kc),
-                 instr_desc_bmn(kM, DVP), (q0 > 0 || kc > 0) ? 1u : 0u);
+                 instr_desc_bmn(kM, DVP), kc > 0);
 #pragma unroll
       for (int kc = 0; kc < kN / 16; ++kc)
         mma_bf16(tmem + kColK, smem_desc(sSt + kc * 256, 128, kN * 16), mndesc(sQk, kc),
-                 instr_desc_bmn(kM, DKP), (q0 > 0 || kc > 0) ? 1u : 0u);
+                 instr_desc_bmn(kM, DKP), kc > 0);
       mma_commit(bar);
     }
     mbar_wait(bar, phase);
     phase ^= 1;
     tc_after_sync();
-  }
-  // tcgen05.ld is warp-collective: every thread loads, only valid keys store
-  const bool any_q = a.s_real > 0;
-  float gv[kHV], gk[kHK];
+    {
+      float bv[kHV], bk[kHK];
+      tmem_ld_cols<kHV>(t_row + kColV + half * kHV, bv);
+      tmem_ld_cols<kHK>(t_row + kColK + half * kHK, bk);
 #pragma unroll
-  for (int t = 0; t < kHV; ++t) gv[t] = 0.f;
+      for (int t = 0; t < kHV; ++t) gv[t] += bv[t];
 #pragma unroll
-  for (int t = 0; t < kHK; ++t) gk[t] = 0.f;
-  if (any_q) {
-    tmem_ld_cols<kHV>(t_row + kColV + half * kHV, gv);
-    tmem_ld_cols<kHK>(t_row + kColK + half * kHK, gk);
+      for (int t = 0; t < kHK; ++t) gk[t] += bk[t];
+    }
   }
+  // tcgen05.ld is warp-collective: every thread loaded, only valid keys store
   if (real) {
 #pragma unroll
     for (int t = 0; t < kHV; ++t) {
