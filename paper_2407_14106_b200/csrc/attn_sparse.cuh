@@ -53,6 +53,11 @@ struct SparseArgs {
   void* dv_out = nullptr;
   void* dbias = nullptr;  // A[E]
   double scale = 1.0;
+  // tile kernels: float(scale) * log2(e) and the row strides in bytes,
+  // computed once on the host (fill_common) so the kernels' main loops read
+  // them as uniform operands instead of rebuilding them every step
+  float scale_l = 0.f;
+  uint32_t rq_bytes = 0, rv_bytes = 0;
   int forbid_empty = 0;
   int vec_qk = 0, vec_v = 0;
   int* err = nullptr;  // [0] non-finite flag, [1] first empty row (atomicMin)

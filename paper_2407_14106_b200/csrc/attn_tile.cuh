@@ -240,14 +240,14 @@ __global__ void __launch_bounds__(kTileThreads, GTE_TILE_MINB) tile_fwd_kernel(S
   TileMeta& mt = *reinterpret_cast<TileMeta*>(smem_raw);
   const TileSmem sm = tile_carve(smem_raw);
   const FastGeom g = fast_geom<T, LPH, LPN>(p.H, p.dk);
-  const float scale_l = float(p.scale) * M::kLogScale;
+  const float scale_l = p.scale_l;  // float(scale) * log2(e), from the host (no per-step F2F)
   const char* Q = static_cast<const char*>(p.q);
   const char* K = static_cast<const char*>(p.k);
   const char* Vp = static_cast<const char*>(p.v);
   const float* __restrict__ wm = static_cast<const float*>(p.wmult);
   char* O = static_cast<char*>(p.out);
   float* __restrict__ LSE = static_cast<float*>(p.lse);
-  const uint32_t rq = (uint32_t)(p.ldq * sizeof(T)), rv = (uint32_t)(p.ldv * sizeof(T));
+  const uint32_t rq = p.rq_bytes, rv = p.rv_bytes;  // row strides in bytes, from the host
 
   const int nrows = tile_stage(mt, sm, p.order, p.tiles, p.row_ptr, p.cols, p.eid,
                                static_cast<const float*>(p.bias));
@@ -374,7 +374,7 @@ __global__ void __launch_bounds__(kTileThreads, GTE_TILE_MINB) tile_bwd_rows_ker
   TileMeta& mt = *reinterpret_cast<TileMeta*>(smem_raw);
   const TileSmem sm = tile_carve(smem_raw);
   const FastGeom g = fast_geom<T, LPH, LPN>(p.H, p.dk);
-  const float scale_l = float(p.scale) * M::kLogScale;
+  const float scale_l = p.scale_l;  // float(scale) * log2(e), from the host (no per-step F2F)
   const char* Q = static_cast<const char*>(p.q);
   const char* K = static_cast<const char*>(p.k);
   const char* Vp = static_cast<const char*>(p.v);
@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(kTileThreads, GTE_TILE_MINB) tile_bwd_rows_ker
   float2* __restrict__ LD = static_cast<float2*>(p.lsedelta);
   char* DQ = static_cast<char*>(p.dq);
   float* __restrict__ DB = static_cast<float*>(p.dbias);
-  const uint32_t rq = (uint32_t)(p.ldq * sizeof(T)), rv = (uint32_t)(p.ldv * sizeof(T));
+  const uint32_t rq = p.rq_bytes, rv = p.rv_bytes;  // row strides in bytes, from the host
 
   const int nrows = tile_stage(mt, sm, p.order, p.tiles, p.row_ptr, p.cols, p.eid,
                                static_cast<const float*>(p.bias));
@@ -509,7 +509,7 @@ __global__ void __launch_bounds__(kTileThreads, GTE_TILE_MINB_COLS) tile_bwd_col
   TileMeta& mt = *reinterpret_cast<TileMeta*>(smem_raw);
   const TileSmem sm = tile_carve(smem_raw);
   const FastGeom g = fast_geom<T, LPH, LPN>(p.H, p.dk);
-  const float scale_l = float(p.scale) * M::kLogScale;
+  const float scale_l = p.scale_l;  // float(scale) * log2(e), from the host (no per-step F2F)
   const char* Q = static_cast<const char*>(p.q);
   const char* K = static_cast<const char*>(p.k);
   const char* Vp = static_cast<const char*>(p.v);
@@ -518,7 +518,7 @@ __global__ void __launch_bounds__(kTileThreads, GTE_TILE_MINB_COLS) tile_bwd_col
   const float2* __restrict__ LD = static_cast<const float2*>(p.lsedelta);
   char* DK = static_cast<char*>(p.dk_out);
   char* DV = static_cast<char*>(p.dv_out);
-  const uint32_t rq = (uint32_t)(p.ldq * sizeof(T)), rv = (uint32_t)(p.ldv * sizeof(T));
+  const uint32_t rq = p.rq_bytes, rv = p.rv_bytes;  // row strides in bytes, from the host
 
   const int nrows = tile_stage(mt, sm, p.order_c, p.tiles_c, p.col_ptr, p.csc_row, p.csc_eid,
                                static_cast<const float*>(p.bias));
@@ -627,13 +627,13 @@ __global__ void __launch_bounds__(kTileThreads) hub_fwd_kernel(SparseArgs p) {
   constexpr int NS = kTileWarps * SLOTS;
   __shared__ float s_m[NS][LPN], s_l[NS][LPN], s_acc[NS][LPN][VW];
   const FastGeom g = fast_geom<T, LPH, LPN>(p.H, p.dk);
-  const float scale_l = float(p.scale) * M::kLogScale;
+  const float scale_l = p.scale_l;  // float(scale) * log2(e), from the host (no per-step F2F)
   const char* Q = static_cast<const char*>(p.q);
   const char* K = static_cast<const char*>(p.k);
   const char* Vp = static_cast<const char*>(p.v);
   const float* __restrict__ bias = static_cast<const float*>(p.bias);
   const float* __restrict__ wm = static_cast<const float*>(p.wmult);
-  const uint32_t rq = (uint32_t)(p.ldq * sizeof(T)), rv = (uint32_t)(p.ldv * sizeof(T));
+  const uint32_t rq = p.rq_bytes, rv = p.rv_bytes;  // row strides in bytes, from the host
   const int i = __ldg(p.hubs + blockIdx.x);
   const int beg = __ldg(p.row_ptr + i), end = __ldg(p.row_ptr + i + 1);
   const int s0 = hub_slot<LPN>(g), w = g.lane % LPN;
@@ -726,13 +726,13 @@ __global__ void __launch_bounds__(kTileThreads) hub_bwd_rows_kernel(SparseArgs p
   constexpr int NS = kTileWarps * SLOTS;
   __shared__ float s_acc[NS][LPN][VW];
   const FastGeom g = fast_geom<T, LPH, LPN>(p.H, p.dk);
-  const float scale_l = float(p.scale) * M::kLogScale;
+  const float scale_l = p.scale_l;  // float(scale) * log2(e), from the host (no per-step F2F)
   const char* K = static_cast<const char*>(p.k);
   const char* Vp = static_cast<const char*>(p.v);
   const float* __restrict__ bias = static_cast<const float*>(p.bias);
   const float* __restrict__ wm = static_cast<const float*>(p.wmult);
   float* __restrict__ DB = static_cast<float*>(p.dbias);
-  const uint32_t rq = (uint32_t)(p.ldq * sizeof(T)), rv = (uint32_t)(p.ldv * sizeof(T));
+  const uint32_t rq = p.rq_bytes, rv = p.rv_bytes;  // row strides in bytes, from the host
   const int i = __ldg(p.hubs + blockIdx.x);
   const int beg = __ldg(p.row_ptr + i), end = __ldg(p.row_ptr + i + 1);
   const int s0 = hub_slot<LPN>(g), w = g.lane % LPN;
@@ -807,13 +807,13 @@ __global__ void __launch_bounds__(kTileThreads) hub_bwd_cols_kernel(SparseArgs p
   constexpr int NS = kTileWarps * SLOTS;
   __shared__ float s_k[NS][LPN][VW], s_v[NS][LPN][VW];
   const FastGeom g = fast_geom<T, LPH, LPN>(p.H, p.dk);
-  const float scale_l = float(p.scale) * M::kLogScale;
+  const float scale_l = p.scale_l;  // float(scale) * log2(e), from the host (no per-step F2F)
   const char* Q = static_cast<const char*>(p.q);
   const char* DO = static_cast<const char*>(p.dout);
   const float* __restrict__ bias = static_cast<const float*>(p.bias);
   const float* __restrict__ wm = static_cast<const float*>(p.wmult);
   const float2* __restrict__ LD = static_cast<const float2*>(p.lsedelta);
-  const uint32_t rq = (uint32_t)(p.ldq * sizeof(T)), rv = (uint32_t)(p.ldv * sizeof(T));
+  const uint32_t rq = p.rq_bytes, rv = p.rv_bytes;  // row strides in bytes, from the host
   const int j = __ldg(p.hubs_c + blockIdx.x);
   const int beg = __ldg(p.col_ptr + j), end = __ldg(p.col_ptr + j + 1);
   const int s0 = hub_slot<LPN>(g), w = g.lane % LPN;

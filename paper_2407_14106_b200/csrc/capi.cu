@@ -434,6 +434,9 @@ void fill_common(SparseArgs& a, const gte_plan* plan, int dtype, int H, int dk, 
   a.csc_row = plan->csc_row;
   a.csc_eid = plan->csc_eid;
   a.scale = 1.0 / std::sqrt((double)dk);
+  a.scale_l = (float)a.scale * 1.4426950408889634f;  // == the kernels' former float(scale) * kLogScale
+  a.rq_bytes = (uint32_t)(ldq * (int64_t)elem_size(dtype));
+  a.rv_bytes = (uint32_t)(ldv * (int64_t)elem_size(dtype));
   a.err = plan->ctx->d_err;
   a.order = plan->order;
   a.tiles = plan->tiles;
