@@ -467,9 +467,9 @@ __global__ void __launch_bounds__(2 * kM, (DKP <= 16 && DVP <= 16) ? 4 : 3)
 #pragma unroll
         for (int i = 0; i < 8; ++i) acc[c8 * 8 + i] = fmaf(acc[c8 * 8 + i], corr, v8[i]);
       }
-      tc_before_sync();
-      __syncthreads();
-      tc_after_sync();
+      // no barrier here: the next block's S MMA is issued after the barrier at
+      // the top of the loop, which every thread reaches only after its O_blk
+      // tcgen05.ld completed
       continue;
     }
     // pass 1: this thread's half-row maximum, combined with the partner's
@@ -548,9 +548,6 @@ __global__ void __launch_bounds__(2 * kM, (DKP <= 16 && DVP <= 16) ? 4 : 3)
 #pragma unroll
       for (int i = 0; i < 8; ++i) acc[c8 * 8 + i] = fmaf(acc[c8 * 8 + i], corr, v8[i]);
     }
-    tc_before_sync();
-    __syncthreads();
-    tc_after_sync();
   }
   // epilogue: row sum = both halves' partial sums
   red[half * kM + rl] = l;
