@@ -365,6 +365,11 @@ def run_sequence_parallel(args, rank, world, local, dist):
         halo_rows = [list(r.boundary_rows()) for r in hp]
     g = torch.Generator(device=dev).manual_seed(99 + rank)
     q, k, v, do = (torch.randn((rows, H * DH), generator=g, device=dev).to(td) for _ in range(4))
+    if args.sp_mode == "halo":  # shards written straight into the layer's [own | halo] buffers
+        views = [layer.own_view(rank, nm, td, dev) for nm in ("q", "k", "v", "do")]
+        for view, x in zip(views, (q, k, v, do)):
+            view.copy_(x)
+        q, k, v, do = views
     flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)

@@ -389,8 +389,23 @@ class HaloAttention:
             if zero_tail:
                 t[r.n_own:].zero_()
             self._bufs[key] = t
-        t[: r.n_own].copy_(own)
+        if own.data_ptr() != t.data_ptr() or own.stride() != t.stride():  # not written in place (own_view)
+            t[: r.n_own].copy_(own)
         return t
+
+    def own_view(self, rank: int, name: str, dtype, device):
+        """The own rows of the persistent [own | halo] buffer of tensor `name`
+        ("q", "k", "v", "do"): a caller that writes a step's shard here saves
+        the per-step copy into the buffer (bench.py's ranks do)."""
+        r = next(x for x in self.ranks if x.rank == rank)
+        key = (rank, name)
+        t = self._bufs.get(key)
+        if t is None or t.dtype != dtype or t.device != device:
+            import torch
+
+            t = torch.zeros((r.n_ext, self.d), dtype=dtype, device=device)
+            self._bufs[key] = t
+        return t[: r.n_own]
 
     def _halo_in_kv(self, kx: dict, vx: dict):
         """Fill the halo tails of the K and V ext buffers with the owners' rows:

@@ -181,3 +181,37 @@ def test_scatter_add_seq_equals_per_peer_adds(cuda, dtype):
     torch.cuda.synchronize()
     assert torch.equal(got, want)
     assert (cnt > 1).any()
+
+
+def test_own_view_inputs_match_copied_inputs(cuda):
+    """Shards written straight into the layer's [own | halo] buffers
+    (HaloAttention.own_view, what bench.py's ranks do) give the results of
+    shards passed as separate tensors, bit for bit."""
+    import torch
+
+    P, H, dh = 3, 8, 8
+    ro, co = community_graph(6000, 10.0, community=128, seed=2, shuffle=False)
+    S, E = ro.shape[0] - 1, co.shape[0]
+    g = torch.Generator(device="cuda").manual_seed(9)
+    q, k, v, up = (torch.randn((S, H * dh), generator=g, device="cuda").to(torch.bfloat16) for _ in range(4))
+    bias = (0.3 * torch.randn(E, generator=g, device="cuda")).float()
+    plans = build_halo_plan(ro, co, P)
+    res = []
+    for in_place in (False, True):
+        layer = HaloAttention(plans, P, H, dh, "bf16", HaloLoopback(P))
+        sh = {}
+        for nm, t in (("q", q), ("k", k), ("v", v), ("do", up)):
+            sh[nm] = {}
+            for r in plans:
+                if in_place:
+                    view = layer.own_view(r.rank, nm, t.dtype, t.device)
+                    view.copy_(t[r.lo:r.hi])
+                    sh[nm][r.rank] = view
+                else:
+                    sh[nm][r.rank] = t[r.lo:r.hi].clone()
+        o = layer.forward(sh["q"], sh["k"], sh["v"], bias)
+        gr = layer.backward(sh["do"])
+        torch.cuda.synchronize()
+        res.append([o[r.rank].clone() for r in plans] + [x.clone() for r in plans for x in gr[r.rank]])
+    for a_, b_ in zip(*res):
+        assert torch.equal(a_, b_)
