@@ -89,6 +89,11 @@ int gte_community_order(int64_t n, int64_t nnz, const int64_t* row_off, const in
                         int64_t* order, int64_t* n_communities);
 int gte_plan_schedule(gte_plan* plan, int64_t iters, int64_t* n_communities);
 int gte_plan_set_order(gte_plan* plan, const int64_t* order);
+/* Rows [n, rows) produce no outputs (forward O / LSE, dQ, the backward's
+ * CSR pass skip them; the CSC pass still covers every column); they must have
+ * no edges. For a sequence-parallel rank's local plan, whose halo rows exist
+ * only as columns (no reference counterpart: an execution-plan option). */
+int gte_plan_set_output_rows(gte_plan* plan, int64_t n);
 
 /* ---- Elastic Computation Reformation on the tensor pipe (the
  * reference's dense sub-blocks, reformation.cpp:111-195, tile spans

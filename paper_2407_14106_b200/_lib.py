@@ -81,6 +81,7 @@ def lib() -> C.CDLL:
             L.gte_community_order.argtypes = [I64, I64, VP, VP, I64, VP, C.POINTER(I64)]
             L.gte_plan_schedule.argtypes = [VP, I64, C.POINTER(I64)]
             L.gte_plan_set_order.argtypes = [VP, VP]
+            L.gte_plan_set_output_rows.argtypes = [VP, I64]
             L.gte_plan_set_blocks.argtypes = [VP, I64, VP, I64, C.POINTER(I64)]
             L.gte_plan_blocks.argtypes = [VP, C.POINTER(I64), C.POINTER(I64)]
             L.gte_sparse_attn_fwd.argtypes = [VP, VP, I32, I32, I32, I32, VP, VP, I64, VP, I64, VP, VP, VP, VP, I32]

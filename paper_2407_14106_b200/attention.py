@@ -192,6 +192,11 @@ class DevicePlan:
             raise ConfigError("plan: order length must equal the row count")
         check(_lib.lib().gte_plan_set_order(self.h, o.ctypes.data))
 
+    def set_output_rows(self, n: int) -> None:
+        """Rows >= n (which must have no edges) produce no outputs: the
+        forward and the backward's CSR pass skip them (gte_plan_set_output_rows)."""
+        check(_lib.lib().gte_plan_set_output_rows(self.h, int(n)))
+
     def set_blocks(self, origins, d_b: int = 16) -> int:
         """Registers ECR sub-blocks (global (row0, col0) origins, side d_b;
         ClusterSparseLayout.global_blocks()): with d_b == 16, bf16 calls run

@@ -166,6 +166,7 @@ struct gte_plan {
   bool scheduled = false;
   int64_t communities = 0;
   std::vector<int64_t> host_order;  // execution order given to gte_plan_set_order (empty: natural)
+  int64_t out_rows = -1;            // gte_plan_set_output_rows: the CSR pass skips rows >= out_rows
   EcrSplit* ecr = nullptr;
 };
 
@@ -289,6 +290,7 @@ int build_exec(gte_plan* p, const int64_t* order) {
     int rows_in = 0, edges_in = 0;
     for (int64_t x = 0; x < n; ++x) {
       const int32_t r = (int32_t)(order ? order[x] : x);
+      if (pass == 0 && p->out_rows >= 0 && r >= p->out_rows) continue;  // no outputs wanted (edge-free rows)
       const int dg = deg(r);
       if (dg > kHubDegree) {
         P.hubs.push_back(r);
@@ -635,6 +637,23 @@ int gte_plan_set_order(gte_plan* p, const int64_t* order) {
   if (order) p->host_order.assign(order, order + n);
   else p->host_order.clear();
   if (p->ecr && p->ecr->rem) return gte_plan_set_order(p->ecr->rem, order);
+  return GTE_OK;
+}
+
+// Rows [n, rows) produce no outputs: the forward and the backward's CSR pass
+// skip them (their O / LSE / dQ rows are left unwritten); they must have no
+// edges. The CSC pass still covers every column. For a sequence-parallel
+// rank's local plan, whose trailing halo rows only exist as columns.
+int gte_plan_set_output_rows(gte_plan* p, int64_t n) {
+  if (!p) return fail(GTE_CONFIG, "plan: null plan");
+  if (n < 0 || n > p->rows) return fail(GTE_CONFIG, "plan: output rows out of range");
+  int32_t off = 0;
+  CUDA_TRY(cudaMemcpy(&off, p->row_ptr + n, sizeof off, cudaMemcpyDeviceToHost));
+  if (off != p->nnz) return fail(GTE_CONFIG, "plan: rows without outputs must have no edges");
+  p->out_rows = n == p->rows ? -1 : n;
+  int rc = build_exec(p, p->host_order.empty() ? nullptr : p->host_order.data());
+  if (rc) return rc;
+  if (p->ecr && p->ecr->rem) return gte_plan_set_output_rows(p->ecr->rem, n);
   return GTE_OK;
 }
 

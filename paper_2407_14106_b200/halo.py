@@ -242,10 +242,12 @@ class DeviceHaloOps:
         self.att = {}
         self._comm = None
 
-    def setup(self, key, n: int, ro: np.ndarray, co: np.ndarray):
+    def setup(self, key, n: int, ro: np.ndarray, co: np.ndarray, n_out: int | None = None):
         plan = DevicePlan.from_host(ro, co, self.ctx)
         if self.schedule:
             plan.schedule()
+        if n_out is not None and n_out < n:  # halo rows exist only as columns: no tiles for them
+            plan.set_output_rows(n_out)
         self.att[key] = DeviceSparseAttention(plan, self.H, self.dh, self.dh, self.dtype)
 
     def index(self, idx: np.ndarray):
@@ -345,12 +347,12 @@ class HaloAttention:
                 for tag in ("i", "b"):
                     ro_, co_, ei = getattr(r, "ro_" + tag), getattr(r, "co_" + tag), getattr(r, "eidx_" + tag)
                     if co_.shape[0]:
-                        self.ops.setup((r.rank, tag), r.n_ext, ro_, co_)
+                        self.ops.setup((r.rank, tag), r.n_ext, ro_, co_, r.n_own)
                         parts.append((tag, torch.tensor(ei, dtype=torch.int64, device=dev)))
                 self.parts[r.rank] = parts
                 self._bmask[r.rank] = torch.tensor(r.boundary, device=dev)
             else:
-                self.ops.setup((r.rank, "all"), r.n_ext, r.local_ro, r.local_co)
+                self.ops.setup((r.rank, "all"), r.n_ext, r.local_ro, r.local_co, r.n_own)
                 self.parts[r.rank] = [("all", None)]
             cat = np.concatenate(r.send_idx) if r.send_idx else np.zeros(0, np.int32)
             self.idx[r.rank] = self.ops.index(cat)

@@ -97,7 +97,7 @@ class CpuHaloOps:
     def __init__(self, orc, H, dh):
         self.orc, self.H, self.dh, self.g = orc, H, dh, {}
 
-    def setup(self, key, n, ro, co):
+    def setup(self, key, n, ro, co, n_out=None):
         from oracle import CSR
 
         self.g[key] = CSR(n, ro, co)
