@@ -215,3 +215,38 @@ def test_own_view_inputs_match_copied_inputs(cuda):
         res.append([o[r.rank].clone() for r in plans] + [x.clone() for r in plans for x in gr[r.rank]])
     for a_, b_ in zip(*res):
         assert torch.equal(a_, b_)
+
+
+def test_plan_output_rows(cuda):
+    """gte_plan_set_output_rows: rows >= n (edge-free) get no forward / CSR-pass
+    work; rows < n and every dK / dV column equal the full plan's bit for bit.
+    Rows >= n with edges are refused (ConfigError)."""
+    import torch
+
+    from paper_2407_14106_b200._lib import ConfigError
+
+    H, dh, n_own, n_halo = 8, 8, 3000, 700
+    rng = np.random.default_rng(4)
+    deg = rng.integers(1, 12, n_own)
+    ro = np.concatenate([[0], np.cumsum(deg), np.full(n_halo, deg.sum())]).astype(np.int64)
+    co = np.concatenate([np.sort(rng.choice(n_own + n_halo, int(d), replace=False)) for d in deg]).astype(np.int64)
+    S, E = n_own + n_halo, co.shape[0]
+    g = torch.Generator(device="cuda").manual_seed(4)
+    q, k, v, up = (torch.randn((S, H * dh), generator=g, device="cuda").to(torch.bfloat16) for _ in range(4))
+    bias = (0.3 * torch.randn(E, generator=g, device="cuda")).float()
+    res = []
+    for limit in (False, True):
+        plan = A.DevicePlan.from_host(ro, co)
+        plan.schedule()
+        if limit:
+            plan.set_output_rows(n_own)
+        att = A.DeviceSparseAttention(plan, H, dh, dh, "bf16")
+        o, lse = att.forward(q, k, v, bias)
+        dq, dk, dv, db = att.backward(q, k, v, o, lse, up, bias)
+        torch.cuda.synchronize()
+        res.append((o[:n_own].clone(), lse[:n_own].clone(), dq[:n_own].clone(), dk.clone(), dv.clone(), db[:E].clone()))
+    for a_, b_ in zip(*res):
+        assert torch.equal(a_, b_)
+    plan = A.DevicePlan.from_host(ro, co)
+    with pytest.raises(ConfigError):
+        plan.set_output_rows(n_own - 1)
