@@ -771,8 +771,40 @@ def main():
             aev[i][1].record(stream)
         torch.cuda.synchronize()
         ams = float(np.mean([x.elapsed_time(y) for x, y in aev]))
+        alaunch = "eager launches"
+        if not args.no_graph:  # the same step as one CUDA graph replay, as for the main dtype
+            def astep():
+                aatt.forward(aq, ak, av, bias, out=ao, lse=al)
+                aatt.backward(aq, ak, av, ao, al, ado, bias, dq=adq, dk=adk, dv=adv, dbias=dbias)
+            try:
+                side = torch.cuda.Stream(device=dev)
+                side.wait_stream(stream)
+                with torch.cuda.stream(side):
+                    astep()
+                stream.wait_stream(side)
+                torch.cuda.synchronize()
+                agraph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(agraph):
+                    astep()
+                ctx.set_stream(stream.cuda_stream)
+                gev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
+                for _ in range(args.warmup):
+                    flush.zero_()
+                    agraph.replay()
+                for i in range(args.steps):
+                    flush.zero_()
+                    gev[i][0].record(stream)
+                    agraph.replay()
+                    gev[i][1].record(stream)
+                torch.cuda.synchronize()
+                ams = float(np.mean([x.elapsed_time(y) for x, y in gev]))
+                alaunch = "one CUDA graph per step (fwd + bwd)"
+            except Exception as exc:  # noqa: BLE001 - keep the eager number
+                ctx.set_stream(stream.cuda_stream)
+                alaunch = f"eager launches (graph capture failed: {type(exc).__name__})"
         aalg = algorithmic_bytes(S, E, ea)
         line["alt_dtype"] = {"dtype": alt, "value": S / (ams * 1e-3), "unit": "nodes/s", "ms_per_step": ams,
+                             "launch": alaunch,
                              "roofline_frac": aalg / (ams * 1e-3) / 1e9 / hbm,
                              "parity": "bf16: max-norm 2e-2 / L2 1e-2 vs the fp64 oracle" if alt == "bf16"
                              else "f32: max-norm and L2 <= 1e-5 vs the fp64 oracle"}
