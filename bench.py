@@ -52,6 +52,17 @@ def algorithmic_bytes(S, E, e):
     return 12 * e * S * H * DH + 8 * S * H + 8 * (S + 1) + 20 * E
 
 
+def algorithmic_bytes_pass(S, E, e):
+    """SURVEY.md §8(d3) split by pass: forward (Q, K, V in, O and LSE out,
+    row offsets, columns + bias) and backward (Q, K, V, O, dO in, dQ, dK, dV
+    out, LSE, offsets, columns + bias in, dbias out); they sum to
+    algorithmic_bytes."""
+    d = H * DH
+    fwd = 4 * e * S * d + 4 * S * H + 4 * (S + 1) + 8 * E
+    bwd = 8 * e * S * d + 4 * S * H + 4 * (S + 1) + 12 * E
+    return fwd, bwd
+
+
 def make_workload(seed=7, pattern="ecr", info=None):
     """C3 sequence -> attention pattern, as the reference Trainer prepares it
     (proj/src/model.cpp:378-392, 437-468): node ids shuffled, cluster-aware
@@ -730,6 +741,13 @@ def main():
                      "kernel": "tile_fwd + tile_bwd_rows + tile_bwd_cols (3 launches per step)",
                      "algorithmic_bytes_per_step": alg},
         "kernels_ms": {"fwd": float(np.mean(fwd_ms)), "bwd": float(np.mean(bwd_ms))},
+        # per pass (eager launches, CUDA events around each): the backward
+        # (tile_bwd_rows + tile_bwd_cols, ~70 % of the step) is the dominant one
+        "roofline_by_pass": {
+            nm: {"algorithmic_bytes": ab, "ms": t, "achieved_gbs": ab / (t * 1e-3) / 1e9,
+                 "frac": ab / (t * 1e-3) / 1e9 / hbm}
+            for nm, ab, t in zip(("fwd", "bwd"), algorithmic_bytes_pass(S, E, e),
+                                 (float(np.mean(fwd_ms)), float(np.mean(bwd_ms))))},
         "launch": launch_note, "eager_ms_per_step": eager_ms,
         # the memory-side quantity the kernels move: bytes the
         # three passes request per step — every pair gathers a full K and V row
