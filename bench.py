@@ -419,7 +419,7 @@ def run_sequence_parallel(args, rank, world, local, dist):
             stream.wait_stream(side)
             torch.cuda.synchronize()
             g_ = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g_):
+            with torch.cuda.graph(g_, capture_error_mode="thread_local"):  # NCCL proxy threads may call CUDA
                 graph_out = step()
             torch.cuda.synchronize()
             graph = g_
