@@ -152,6 +152,21 @@ __device__ __forceinline__ uint4 ldg16(const char* base, uint32_t off) {
   return __ldg(reinterpret_cast<const uint4*>(base + off));
 }
 
+// This lane's piece of row 0 of a row-major tensor in a 64-bit register (the
+// empty asm keeps the compiler from re-adding the uniform tensor base after
+// the row offset): a gather is then one IMAD.WIDE.U32 (row * stride + base)
+// instead of a multiply and a 64-bit add. Costs two live registers; it pays
+// in the bf16 forward only (profiles/r2l: the backward passes and the f32
+// kernels lose more to the 64-register allocation than they save).
+__device__ __forceinline__ const char* lane_base(const char* base, uint32_t bo) {
+  const char* b = base + bo;
+  asm("" : "+l"(b));
+  return b;
+}
+__device__ __forceinline__ uint4 ldg16r(const char* lane_row0, uint32_t row, uint32_t stride) {
+  return __ldg(reinterpret_cast<const uint4*>(lane_row0 + (uint64_t)row * stride));
+}
+
 template <int LPH>
 __device__ __forceinline__ float head_sum(float x) {
 #pragma unroll

@@ -32,6 +32,8 @@
 // (forward) or partial sums (backward), merged through shared memory.
 #pragma once
 
+#include <type_traits>
+
 #include "attn_piece.cuh"
 
 namespace gte_b200 {
@@ -248,6 +250,9 @@ __global__ void __launch_bounds__(kTileThreads, GTE_TILE_MINB) tile_fwd_kernel(S
   char* O = static_cast<char*>(p.out);
   float* __restrict__ LSE = static_cast<float*>(p.lse);
   const uint32_t rq = p.rq_bytes, rv = p.rv_bytes;  // row strides in bytes, from the host
+  constexpr bool kLaneBase = std::is_same<T, __nv_bfloat16>::value;
+  const char* Kl = lane_base(K, g.bo);
+  const char* Vl = lane_base(Vp, g.bo);
 
   const int nrows = tile_stage(mt, sm, p.order, p.tiles, p.row_ptr, p.cols, p.eid,
                                static_cast<const float*>(p.bias));
@@ -308,8 +313,13 @@ __global__ void __launch_bounds__(kTileThreads, GTE_TILE_MINB) tile_fwd_kernel(S
       const int jj = sm.cols[base + u];
       bl[u] = sm.bias[base + u];
       const uint32_t j = (uint32_t)jj;
-      kr[u] = ldg16(K, j * rq + g.bo);
-      vr[u] = ldg16(Vp, j * rv + g.bo);
+      if constexpr (kLaneBase) {
+        kr[u] = ldg16r(Kl, j, rq);
+        vr[u] = ldg16r(Vl, j, rv);
+      } else {
+        kr[u] = ldg16(K, j * rq + g.bo);
+        vr[u] = ldg16(Vp, j * rv + g.bo);
+      }
     }
     float s[EPL];
 #pragma unroll
