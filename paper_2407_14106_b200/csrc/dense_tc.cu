@@ -268,9 +268,10 @@ __device__ __forceinline__ void fwd_stage_kv(const TcArgs& a, const CUtensorMap*
 // output columns. Twice the warps of a 4-warp tile at the same TMEM budget
 // (128 columns per CTA, 4 CTAs per SM), for latency hiding.
 template <int DKP, int DVP, bool BW>  // BW: a bias or a weight_mult is present
-// dh <= 16: 4 CTAs per SM (64 registers, TMEM 4 x 128 columns; measured
-// -3.4 % vs 3 CTAs at S = 32,768 despite a small spill); wider heads keep 3
-__global__ void __launch_bounds__(2 * kM, (DKP <= 16 && DVP <= 16) ? 4 : 3)
+// 3 CTAs per SM (85 registers, no spills). With the cp.async staging 4 CTAs
+// at 64 registers were 3.4 % faster for dh <= 16 (r2m); since the TMA
+// staging and the one-pass softmax, 3 are 0.75 % faster (profiles/r2ay)
+__global__ void __launch_bounds__(2 * kM, 3)
     dense_tc_fwd_kernel(TcArgs a, const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV) {
   constexpr int kT = 2 * kM;     // threads
   constexpr int kHalfN = kN / 2; // key columns per thread
